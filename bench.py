@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: signals/s of one SBO iteration (p=64, K=16, s0=8) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one ``sbo_train`` loop-body iteration (sbo.py:352-397) entering with
+K-1 = 15 blocks and leaving with K = 16, over m = 2^20 synthetic 8x8 image
+patches per GPU (BASELINE.json config B; weak scaling across ranks, signals
+sharded by contiguous columns).  Every step restores the same entering state.
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the reference
+algorithm on the host cores instead (the CPU oracle port; rank 0 only).
+"""
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import math  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import time  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "signals/sec per SBO iteration (p=64,K=16,s0=8) at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--m", type=int, default=1 << 20, help="signals per GPU")
+    ap.add_argument("--p-edge", type=int, default=8)
+    ap.add_argument("--K", type=int, default=16)
+    ap.add_argument("--s0", type=int, default=8)
+    ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--scene", type=int, default=2048)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 17)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(a, world):
+    return (f"B: p={a.p_edge**2}, K={a.K} (entering {a.K - 1}), s0={a.s0}, R={a.rounds}, "
+            f"m=2^{int(math.log2(a.m))} per GPU x {world}, W=m/16, 8x8 patches of a "
+            f"{a.scene}^2 synthetic scene")
+
+
+def shard_signals(a, rank, world):
+    from paper_1412_4944_b200 import signals
+    m_total = a.m * world
+    grid = signals.scene(a.scene, a.scene, 0)
+    u8 = signals.patch_bytes(grid, a.p_edge, m_total, 11)
+    lo, hi = rank * a.m, (rank + 1) * a.m
+    return signals.unit_range(u8[lo:hi]), m_total
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc = index, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def iteration_model(p, K, s0, R, w_frac):
+    """SURVEY.md §8(d) algorithmic FLOPs and bytes per signal of one iteration."""
+    flops = 2 * p * p * (K + R) + 2 * p * s0 * R + w_frac * (2 * p * p * (R + 1) + 2 * p * s0 * R)
+    bytes_ = 4 * p * (R + 2) + 4 * p * (R + 1) * w_frac + 4 * (10 + 5 * s0)
+    return flops, bytes_
+
+
+# --------------------------------------------------------------------------- CPU
+def cpu_iteration_sample(a, y_rows, blocks, workers):
+    """Time the reference algorithm (oracle port) on a bounded sample of the workload."""
+    from oracle import sbo_oracle as O
+    y = y_rows.T.astype(np.float64)
+    p, m = y.shape
+    rep0 = O.code_signals(y, blocks, a.s0, workers=workers)
+    w = max(p, m // 16)
+    t0 = time.perf_counter()
+    O.iterate(y, blocks, rep0.residual_sq, a.s0, a.rounds, w, seed=1, workers=workers)
+    return time.perf_counter() - t0
+
+
+def run_reference(a):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import sbo_oracle as O
+    from paper_1412_4944_b200 import signals
+    workers = os.cpu_count() or 1
+    grid = signals.scene(a.scene, a.scene, 0)
+    rows = signals.unit_range(signals.patch_bytes(grid, a.p_edge, a.cpu_sample, 11))
+    y = rows.T.astype(np.float64)
+    p, m = y.shape
+    blocks = O.initial_blocks(y, a.s0, a.K - 1, 4096, a.rounds, seed=1, workers=workers)
+    rep0 = O.code_signals(y, blocks, a.s0, workers=workers)
+    w = max(p, m // 16)
+    times = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        O.iterate(y, blocks, rep0.residual_sq, a.s0, a.rounds, w, seed=1, workers=workers)
+        if i >= a.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    v = m / t
+    sample = (f"one iteration on the first {m} signals of the same workload (p={p}, "
+              f"K={a.K - 1}->{a.K}, s0={a.s0}, R={a.rounds}, W=m/16); numpy/OpenBLAS, "
+              f"OPENBLAS_NUM_THREADS=1, thread pool of {workers}")
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "signals/s", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": workload_name(a, a.gpus), "sample_m": m},
+        "cpu_baseline": {"value": v, "unit": "signals/s", "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "signals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU
+KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1,
+                    "sbo_outer_segments": 1, "sbo_reduce_segments": 1, "sbo_polar": 1,
+                    "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_residual": 2,
+                    "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2}
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1412_4944_b200.engine import Comm, Engine, Signals, TorchComm, require_device
+    from paper_1412_4944_b200.sbo import SboConfig, _block_rng, _init_into
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = require_device(local)
+    comm = Comm()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = TorchComm()
+    rows, m_total = shard_signals(a, rank, world)
+    p = rows.shape[1]
+    eng = Engine(Signals.from_rows(rows, dev), a.s0, k_cap=a.K, comm=comm, m_total=m_total)
+    lo = rank * a.m
+
+    def local_cols(cols):
+        sel = cols[(cols >= lo) & (cols < lo + a.m)]
+        return sel - lo
+
+    cfg = SboConfig(s0=a.s0, k0=a.K - 1, p0=4096, rounds=a.rounds, k_max=a.K, seed=1)
+    _init_into(eng, cfg, m_total, local_cols if world > 1 else None)
+    eng.represent_full()
+    torch.cuda.synchronize()
+    snap_blocks = eng.blocks.clone()
+    st = eng.state
+    snap = [t.clone() for t in (st.best, st.score, st.kept, st.norm, st.residual, st.total)]
+    K0 = eng.K
+    draws = _block_rng(1, 1, K0).standard_normal((p + 8, p))
+    w = max(p, m_total // 16)
+
+    def restore():
+        eng.blocks.copy_(snap_blocks)
+        for dst, src in zip((st.best, st.score, st.kept, st.norm, st.residual, st.total), snap):
+            dst.copy_(src)
+        eng.K = K0
+
+    class Marks:
+        def __init__(self):
+            self.ev = []
+
+        def mark(self):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev.append(e)
+
+    for _ in range(a.warmup):
+        restore()
+        eng.iterate(w, a.rounds, draws)
+    # count launches inside the timed region
+    calls = {}
+    orig = eng._call
+
+    def counting(name, *args):
+        calls[name] = calls.get(name, 0) + 1
+        return orig(name, *args)
+
+    eng._call = counting
+    sampler = ClockSampler(local)
+    marks = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(a.steps):
+        restore()
+        mk = Marks()
+        out = eng.iterate(w, a.rounds, draws, timer=mk)
+        marks.append(mk)
+    t_end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    eng._call = orig
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    el = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    elapsed = float(el.item())
+    t_step = elapsed / a.steps
+    value = m_total / t_step
+    launches = sum(KERNELS_PER_CALL.get(n, 1) * c for n, c in calls.items())
+    # dominant kernel: the full energy pass of represent #2 (events inside the timed region)
+    rep2 = [mk.ev[3].elapsed_time(mk.ev[4]) / 1e3 for mk in marks]
+    t_rep2 = float(np.mean(rep2))
+    hbm, bf16, src = peaks()
+    flops_energy = 2.0 * p * p * a.K * a.m
+    achieved = flops_energy / t_rep2 / 1e12
+    f_sig, b_sig = iteration_model(p, a.K, a.s0, a.rounds, 1.0 / 16)
+    t_roof = max(f_sig * a.m / (bf16 / 2 * 1e12), b_sig * a.m / (hbm * 1e9))
+    phases = np.mean([[mk.ev[i].elapsed_time(mk.ev[i + 1]) for i in range(4)] for mk in marks],
+                     axis=0)
+
+    # e2e: host buffers through the public engine API, copies inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist if world > 1 else None)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        n = min(a.cpu_sample, rows.shape[0])
+        blocks = [q for q in snap_blocks[:K0].cpu().numpy()]
+        t = cpu_iteration_sample(a, rows[:n], blocks, workers)
+        cpu = {"value": n / t, "unit": "signals/s", "cores": workers, "kind": "port",
+               "sample": f"one iteration on the first {n} signals of the workload, oracle port "
+                         f"(numpy/OpenBLAS 1 thread + {workers}-thread pool), same entering "
+                         f"blocks"}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "signals/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded procedural scene, 8x8 patches, float32 signals)",
+        "config": {"workload": workload_name(a, world), "p": p, "K": a.K, "s0": a.s0,
+                   "rounds": a.rounds, "m_per_gpu": a.m, "W": w,
+                   "l2": "inputs larger than L2 (fp32 signals 4*p*m bytes per GPU, 256 MB at m=2^20 > 126 MB L2)",
+                   "parallelism": f"column shards over {world} GPU(s), NCCL allreduce"},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "phases_ms": {"worst+new_block": phases[0], "represent1": phases[1],
+                      "group+retrain": phases[2], "represent2": phases[3]},
+        "roofline": {"kernel": "k_energy_f64 (represent #2 energy/argmax pass)",
+                     "bound": "tensor", "achieved": achieved, "peak": bf16,
+                     "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
+                     "peak_source": f"{src} bf16 dense (TF32 dense = peak/2)",
+                     "algorithmic": f"2*p^2*K flop/signal x {a.m} signals per launch"},
+        "iteration_roofline": {"flop_per_signal": f_sig, "bytes_per_signal": b_sig,
+                               "t_roof_ms": t_roof * 1e3, "frac": t_roof / t_step,
+                               "model": "SURVEY.md 8(d): max(F/TF32 peak, B/HBM)"},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "rmse": out.rmse,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
+    """Same metric through the host-buffer path: H2D of the step's signals and entering
+    state, the iteration, D2H of the new dictionary and assignment."""
+    import torch
+    st = eng.state
+    host_y = torch.from_numpy(rows).pin_memory()
+    host_blocks = snap_blocks[:K0].cpu().pin_memory()
+    host_state = [t.cpu().pin_memory() for t in snap]
+    out_blocks = torch.empty((K0 + 1,) + tuple(snap_blocks.shape[1:]), dtype=torch.float64).pin_memory()
+    out_best = torch.empty(rows.shape[0], dtype=torch.int32).pin_memory()
+    out_res = torch.empty(rows.shape[0], dtype=torch.float64).pin_memory()
+    h2d = host_y.numel() * 4 + host_blocks.numel() * 8 + sum(t.numel() * t.element_size()
+                                                            for t in host_state)
+    d2h = out_blocks.numel() * 8 + out_best.numel() * 4 + out_res.numel() * 8
+
+    def step():
+        eng.sig.y.copy_(host_y, non_blocking=True)
+        eng.blocks[:K0].copy_(host_blocks, non_blocking=True)
+        for dst, src in zip((st.best, st.score, st.kept, st.norm, st.residual, st.total),
+                            host_state):
+            dst.copy_(src, non_blocking=True)
+        eng.K = K0
+        eng.iterate(w, a.rounds, draws)
+        out_blocks.copy_(eng.blocks[: K0 + 1], non_blocking=True)
+        out_best.copy_(st.best, non_blocking=True)
+        out_res.copy_(st.residual, non_blocking=True)
+
+    step()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(a.steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([s.elapsed_time(e) / 1e3 / a.steps], dtype=torch.float64,
+                     device=eng.dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    m_total = eng.m_total
+    return {"value": m_total / float(t.item()), "unit": "signals/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,214 @@
+/*
+ * sbo_b200.h — C ABI of the B200-native SBO iteration (arXiv 1412.4944).
+ *
+ * The library (paper_1412_4944_b200/libsbo_b200.so) exports the device
+ * operations one Single-Block-Orthogonal dictionary-learning iteration is made
+ * of.  Every entry point takes plain DEVICE pointers, sizes and a cudaStream_t
+ * passed as void*; all work is stream-ordered and asynchronous.  No torch
+ * types cross this boundary.  Each function names the reference function it
+ * replaces (paths relative to /root/reference/pkg/src/orthodict/).
+ *
+ * Layouts (device):
+ *   signals  y      : float32 or float64 (dtype), m rows of p  (signal j = y[j*p .. j*p+p-1]; this is the
+ *                     reference's column-major p x m matrix, one contiguous column per signal)
+ *   blocks   Q      : float64, K row-major p x p matrices (Q_b[k][i] = blocks[b*p*p + k*p + i];
+ *                     atom i of block b is column i, exactly numpy's C-order block)
+ *   codes  idx/val  : int16 / float64, k = min(s0, p) rows of a row stride `ld`
+ *                     (row r, column j at r*ld + j; indices ascending down a column)
+ *
+ * Return value: SBO_OK or an error code; sbo_last_error() gives the message.
+ * Numerical failures detected on the device (orthonormality defect > 1e-8,
+ * Jacobi non-convergence) are reported through the int32 `status` arrays the
+ * caller owns, so that a whole iteration can be enqueued without host syncs.
+ */
+#ifndef SBO_B200_H
+#define SBO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SBO_OK = 0,
+  SBO_EINVAL = 1,       /* bad argument              -> ValueError          */
+  SBO_ENUMERICAL = 2,   /* defect > 1e-8             -> NumericalError      */
+  SBO_EDECOMP = 3,      /* SVD/eig did not converge  -> DecompositionError  */
+  SBO_ECUDA = 4         /* CUDA launch/runtime error -> RuntimeError        */
+};
+
+enum { SBO_KIND_SQUARED_SUM = 0, SBO_KIND_ABS_SUM = 1 }; /* sbo.py:31 */
+
+/* element type of the signal matrix: float32 (the fast path; exact whenever the
+ * caller's float64 signals are float32-representable) or float64 (bit-faithful
+ * to arbitrary float64 inputs). */
+enum { SBO_F32 = 0, SBO_F64 = 1 };
+
+/* per-block device status words written by sbo_polar / sbo_init_block */
+enum { SBO_ST_OK = 0, SBO_ST_SKIPPED = 1, SBO_ST_DEFECT = 2, SBO_ST_NOCONV = 3 };
+
+int sbo_abi_version(void);
+const char* sbo_last_error(void);
+/* 1 when the calling process has a usable sm_100 device */
+int sbo_device_ok(int device);
+
+/* ---------------------------------------------------------------------------
+ * Representation, energy pass — replaces sbo.py:177-194 (represent, pass 1) and
+ * the per-block scoring of sbo.py:126-135 (block_energy).
+ * For every signal j < m and block b in [b0, b1): c = Q_b^T y_j, score =
+ * sum of the k largest c^2 (kind 0) or |c| (kind 1); the winner is the first
+ * maximum.  accumulate = 0: fresh pass (b0 must be 0).  accumulate = 1: the
+ * incoming (best, score, kept_sq) describe blocks [0, b0) and a block in
+ * [b0, b1) replaces the winner only with a strictly larger score — the
+ * incremental pass after a block is appended (sbo.py:357-363).
+ * Outputs per signal: best block, its score, its kept sum of squares, ||y||^2.
+ */
+int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* blocks, int b0, int b1,
+                    int s0, int kind, int accumulate, int32_t* best, double* score,
+                    double* kept_sq, double* norm_sq, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Stable grouping by block — replaces sbo.py:231-249 (group_by_block) and the
+ * argsort/searchsorted of sbo.py:200-201.  perm lists signals block by block,
+ * original order inside a block; bounds[b] .. bounds[b+1] is block b's range.
+ * Also emits the segment table used by the per-block kernels: every block's
+ * range split into chunks of at most `seg_len` signals (seg_len multiple of 64).
+ * Workspace: sbo_group_workspace_bytes(m, K).
+ */
+size_t sbo_group_workspace_bytes(int64_t m, int K);
+int64_t sbo_max_segments(int64_t m, int K, int seg_len);
+int sbo_group(const int32_t* best, int64_t m, int K, int seg_len, int32_t* perm,
+              int64_t* bounds, int32_t* seg_block, int64_t* seg_lo, int64_t* seg_hi,
+              int32_t* nseg, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Own-block coding — replaces onb.py:58-76 (select_top) applied to Q_b^T y as in
+ * sbo.py:203-209 (represent pass 2) and onb.py:170 (train_onb coding step).
+ * Segments from sbo_group (or a single segment over a member list).  For the
+ * signal at order[t] (t in a segment of block b): its k kept indices (ascending)
+ * and values are written at column `t` (out_by_signal = 0) or at column
+ * order[t] (out_by_signal = 1) of idx/val (row stride ld).  energy/kept_sq
+ * (optional, indexed like the codes) receive the score and sum of squares of
+ * the kept values (sbo.py:213-217).  block_override >= 0 codes every segment
+ * against that block instead of seg_block.
+ */
+int sbo_code_segments(const void* y, int dtype, int p, const int32_t* order, const int32_t* seg_block,
+                      const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
+                      int64_t max_seg, const double* blocks, int block_override, int s0,
+                      int kind, int out_by_signal, int64_t ld, int16_t* idx, double* val,
+                      double* energy, double* kept_sq, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Sparse outer product P = Y X^T per segment — replaces onb.py:127-134
+ * (sparse_outer).  Codes are read at column t of the segment order (the layout
+ * sbo_code_segments writes with out_by_signal = 0).  partial receives one
+ * float64 p x p matrix per segment (row-major, P[k][i] = sum y[k] x[i]);
+ * sbo_reduce_segments sums the partials of each block in segment order
+ * (deterministic) into P (K x p x p).  counts (optional, K int64) receives
+ * bounds-derived signal counts per block.
+ */
+int sbo_outer_segments(const void* y, int dtype, int p, const int32_t* order, const int64_t* seg_lo,
+                       const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg, int s0,
+                       int64_t ld, const int16_t* idx, const double* val, double* partial,
+                       void* stream);
+int sbo_reduce_segments(const double* partial, const int32_t* seg_block, const int32_t* nseg,
+                        int64_t max_seg, int K, int p, double* P, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Gram matrix G = Y_W Y_W^T of a member list (float64) — the data term of the
+ * new block's initialisation (onb.py:79-95 via thin_svd(ysub), linalg.py:52).
+ * Partials: one p x p matrix per chunk of `chunk` members, reduced in order.
+ * Workspace: sbo_gram_workspace_bytes(w, chunk, p).
+ */
+size_t sbo_gram_workspace_bytes(int64_t w, int chunk, int p);
+int sbo_gram(const void* y, int dtype, int p, const int32_t* members, int64_t w, int chunk,
+             double* G, void* ws, size_t ws_bytes, void* stream);
+
+/* select_top on explicit float64 coefficient vectors (onb.py:58-76): vector j
+ * is row j of coeffs (t x p); codes written at column j (row stride ld). */
+int sbo_select_top(const double* coeffs, int64_t t, int p, int s0, int64_t ld, int16_t* idx,
+                   double* val, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Polar update Q_b = U V^T of P_b for the blocks whose count > 0 — replaces
+ * linalg.py:68-78 (procrustes_polar via thin_svd/gesdd) and the guard of
+ * onb.py:119-124.  One-sided Jacobi (Hestenes) in float64.  Q (K x p x p) is
+ * updated in place; blocks with counts[b] == 0 (counts may be NULL) are left
+ * unchanged and flagged SBO_ST_SKIPPED (sbo.py:379-383).  sigma (optional,
+ * K x p) receives the singular values in descending order.
+ * Workspace: sbo_polar_workspace_bytes(K, p).
+ */
+size_t sbo_polar_workspace_bytes(int K, int p);
+int sbo_polar(const double* P, int K, int p, const int64_t* counts, double* Q, double* sigma,
+              int32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * New block initialisation from a Gram matrix — replaces onb.py:79-116
+ * (init_onb + _complete_columns) with thin_svd's canonical signs
+ * (linalg.py:32-37).  Eigenvectors of G in descending eigenvalue order, each
+ * column's largest-|entry| made nonnegative; directions with
+ * sqrt(lambda_i) <= 1e-12 sqrt(lambda_0) — or below the float64 resolution of
+ * the Gram route, lambda_i <= 64 eps lambda_0 — are replaced by the twice-
+ * projected Gram–Schmidt completion against the host-drawn normals `draws`
+ * (ndraws x p, the block stream's standard_normal draws in order).
+ * ncols < p (fewer members than dimensions) keeps at most ncols directions.
+ * rank (optional, 2 x int32) receives the number of kept directions and the
+ * number of completion draws consumed.
+ */
+size_t sbo_init_workspace_bytes(int p);
+int sbo_init_block(const double* G, int p, int64_t ncols, const double* draws, int ndraws,
+                   double* Q, int32_t* rank, int32_t* status, void* ws, size_t ws_bytes,
+                   void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Thin SVD of a rows x cols float64 matrix with rows >= cols (callers transpose
+ * wide inputs) — replaces linalg.py:40-65 (thin_svd: gesdd/gesvd + canonical
+ * signs).  Outputs row-major U (rows x cols), S (cols, descending) and
+ * V (cols x cols) with A = U diag(S) V^T.  status: SBO_ST_OK / SBO_ST_NOCONV.
+ */
+size_t sbo_svd_workspace_bytes(int rows, int cols);
+int sbo_svd(const double* A, int rows, int cols, double* U, double* S, double* V,
+            int32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Worst-represented set — replaces sbo.py:223-228 (worst_set).  The members of
+ * the w largest residual_sq (ties toward low signal index), written in
+ * ascending signal order to members[0 .. min(w, m)).  Radix select on the
+ * float64 keys.  Workspace: sbo_worst_workspace_bytes(m).
+ * The split form exposes the radix passes for a multi-GPU select: a histogram
+ * of the 256 digit values at `shift` among keys whose bits above shift+8 equal
+ * `prefix` (key_hist), and the final member compaction given the threshold key
+ * and the number of threshold-equal members to keep (worst_collect).
+ */
+size_t sbo_worst_workspace_bytes(int64_t m);
+int sbo_worst_set(const double* residual_sq, int64_t m, int64_t w, int32_t* members,
+                  void* ws, size_t ws_bytes, void* stream);
+int sbo_key_histogram(const double* residual_sq, int64_t m, uint64_t prefix, int shift,
+                      int64_t* hist256, void* stream);
+int sbo_worst_collect(const double* residual_sq, int64_t m, uint64_t threshold_key,
+                      int64_t take_equal, int32_t* members, int64_t* count, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Deterministic float64 sums — sbo.py:295-296 (_rmse numerator) and
+ * linalg.py:89-102 (frobenius_error via explicit residuals).
+ * residual_sq[j] = max(norm_sq[j] - kept_sq[j], 0); *total = sum in fixed order.
+ */
+int sbo_residual(const double* norm_sq, const double* kept_sq, int64_t m, double* residual_sq,
+                 double* total, void* ws, size_t ws_bytes, void* stream);
+size_t sbo_sum_workspace_bytes(int64_t n);
+
+/* ||Q_b^T Q_b - I||_F for K blocks (linalg.py:81-86). */
+int sbo_defect(const double* Q, int K, int p, double* out, void* stream);
+
+/* Exact reconstruction error sum_j ||y_j - Q_{b_j} x_j||^2 (linalg.py:148-162). */
+int sbo_frobenius_sq(const void* y, int dtype, int64_t m, int p, const double* blocks,
+                     const int32_t* block, int s0, int64_t ld, const int16_t* idx,
+                     const double* val, double* total, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBO_B200_H */

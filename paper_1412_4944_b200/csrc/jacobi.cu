@@ -1,0 +1,482 @@
+// Batched one-sided (Hestenes) Jacobi in float64, one CTA per p x p matrix.
+//
+//  * sbo_polar:      Q_b = U V^T of P_b  (linalg.py:68-78 procrustes_polar; the
+//                    reference calls LAPACK gesdd, linalg.py:52) + the
+//                    orthonormality guard of onb.py:119-124.
+//  * sbo_init_block: eigenvectors of the Gram matrix of the worst set, i.e. the
+//                    left singular vectors of ysub (onb.py:79-95 init_onb), with
+//                    descending order and canonical signs (linalg.py:32-37) and
+//                    the seeded Gram–Schmidt completion (onb.py:98-116).
+//
+// Columns of the working matrix A (and of the rotation accumulator V) are
+// stored contiguously (column-major).  A round-robin tournament gives p/2
+// disjoint column pairs per step; each pair is handled by g = 256/(p/2) lanes
+// (capped at a warp) that reduce alpha = |a_i|^2, beta = |a_j|^2, gamma = a_i.a_j
+// with shuffles and apply the Rutishauser rotation.  A sweep without a rotation
+// (|gamma| <= tol sqrt(alpha beta) everywhere) ends the iteration.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace sbo {
+
+constexpr int kJacobiThreads = 256;
+constexpr int kMaxSweeps = 60;
+
+__device__ __forceinline__ double jacobi_tol(int p) { return 4.0 * (p < 16 ? 16 : p) * DBL_EPSILON; }
+
+// Runs the sweeps on A (p x p, col-major) accumulating V.  Returns the sweep
+// count, or -1 when kMaxSweeps is exhausted.  All threads of the CTA call it.
+__device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
+  const int n = p + (p & 1);
+  const int npairs = n >> 1;
+  int g = 32;
+  while (g > 1 && npairs * g > kJacobiThreads) g >>= 1;
+  const int per_round = kJacobiThreads / g;  // pairs handled concurrently
+  const int tid = threadIdx.x;
+  const int lg = tid & (g - 1);
+  const double tol = jacobi_tol(rows > p ? rows : p);
+  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    for (int step = 0; step < n - 1; ++step) {
+      for (int q0 = 0; q0 < npairs; q0 += per_round) {
+        const int q = q0 + tid / g;
+        int i = -1, j = -1;
+        if (q < npairs) {
+          if (q == 0) {
+            i = step;
+            j = n - 1;
+          } else {
+            i = (step + q) % (n - 1);
+            j = (step - q + n - 1) % (n - 1);
+          }
+          if (i >= p || j >= p) i = j = -1;
+        }
+        double al = 0.0, be = 0.0, ga = 0.0;
+        if (i >= 0) {
+          const double* ai = A + static_cast<int64_t>(i) * rows;
+          const double* aj = A + static_cast<int64_t>(j) * rows;
+          for (int r = lg; r < rows; r += g) {
+            const double x = ai[r], y = aj[r];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
+        }
+        for (int o = g >> 1; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (i >= 0 && al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = 1.0 / sqrt(fma(t, t, 1.0));
+          const double s = c * t;
+          double* ai = A + static_cast<int64_t>(i) * rows;
+          double* aj = A + static_cast<int64_t>(j) * rows;
+          double* vi = V + static_cast<int64_t>(i) * p;
+          double* vj = V + static_cast<int64_t>(j) * p;
+          for (int r = lg; r < rows; r += g) {
+            const double x = ai[r], y = aj[r];
+            ai[r] = c * x - s * y;
+            aj[r] = s * x + c * y;
+          }
+          for (int r = lg; r < p; r += g) {
+            const double u = vi[r], w = vj[r];
+            vi[r] = c * u - s * w;
+            vj[r] = s * u + c * w;
+          }
+          if (lg == 0) *flag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) return sweep + 1;
+    __syncthreads();
+  }
+  return -1;
+}
+
+// norms of the columns of A -> sig[j]; descending order with index tie-break -> ord
+__device__ void column_order(const double* A, int rows, int p, double* sig, int* ord,
+                             bool sqrt_norm) {
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    const double* a = A + static_cast<int64_t>(j) * rows;
+    double acc = 0.0;
+    for (int r = 0; r < rows; ++r) acc = fma(a[r], a[r], acc);
+    sig[j] = sqrt_norm ? sqrt(acc) : acc;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    int rank = 0;
+    for (int l = 0; l < p; ++l) rank += (sig[l] > sig[j]) || (sig[l] == sig[j] && l < j);
+    ord[rank] = j;
+  }
+  __syncthreads();
+}
+
+// orthonormality defect of a row-major p x p matrix (CTA-wide, deterministic)
+__device__ double defect_of(const double* Q, int p, double* red) {
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int a = e / p, b = e % p;
+    double g = 0.0;
+    for (int k = 0; k < p; ++k) g = fma(Q[k * p + a], Q[k * p + b], g);
+    g -= (a == b) ? 1.0 : 0.0;
+    acc = fma(g, g, acc);
+  }
+  return sqrt(block_sum<kJacobiThreads>(acc, red));
+}
+
+// ---------------------------------------------------------------------------
+struct JacobiSmem {
+  double red[32];
+  int flag;
+  int count;
+};
+
+__global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restrict__ P, int p,
+                                                          const int64_t* __restrict__ counts,
+                                                          double* Q, double* sigma_out,
+                                                          int32_t* status, double* ws,
+                                                          int use_smem) {
+  const int b = blockIdx.x;
+  const int64_t pp = static_cast<int64_t>(p) * p;
+  __shared__ JacobiSmem S;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  if (counts && counts[b] == 0) {
+    if (threadIdx.x == 0 && status) status[b] = SBO_ST_SKIPPED;
+    return;
+  }
+  double* A;
+  double* V;
+  double* sig;
+  int* ord;
+  if (use_smem) {
+    A = reinterpret_cast<double*>(dyn);
+    V = A + pp;
+    sig = V + pp;
+    ord = reinterpret_cast<int*>(sig + p);
+  } else {
+    A = ws + b * (2 * pp + 2 * p);
+    V = A + pp;
+    sig = V + pp;
+    ord = reinterpret_cast<int*>(sig + p);
+  }
+  const double* Pb = P + b * pp;
+  // A = P in column-major (a_j = column j of P); V = I
+  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+    const int r = static_cast<int>(e / p), c = static_cast<int>(e % p);
+    A[static_cast<int64_t>(c) * p + r] = Pb[e];
+    V[static_cast<int64_t>(c) * p + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int sweeps = jacobi_sweeps(A, V, p, p, &S.flag);
+  column_order(A, p, p, sig, ord, true);
+  const double smax = sig[ord[0]];
+  const double null_tol = smax * 64.0 * DBL_EPSILON;
+  // U_j = a_j / sigma_j in place; null directions completed deterministically
+  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+    const int j = static_cast<int>(e / p);
+    if (sig[j] > null_tol) A[e] /= sig[j];
+  }
+  __syncthreads();
+  for (int rnk = 0; rnk < p; ++rnk) {
+    const int j = ord[rnk];
+    if (sig[j] > null_tol) continue;
+    double* u = A + static_cast<int64_t>(j) * p;
+    for (int cand = 0; cand < p; ++cand) {
+      for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] = (r == cand) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int l = 0; l < p; ++l) {
+          const int jl = ord[l];
+          if (jl == j || (sig[jl] <= null_tol && l > rnk)) continue;
+          const double* w = A + static_cast<int64_t>(jl) * p;
+          double d = 0.0;
+          for (int r = threadIdx.x; r < p; r += blockDim.x) d = fma(w[r], u[r], d);
+          d = block_sum<kJacobiThreads>(d, S.red);
+          for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] -= d * w[r];
+          __syncthreads();
+        }
+      }
+      double nn = 0.0;
+      for (int r = threadIdx.x; r < p; r += blockDim.x) nn = fma(u[r], u[r], nn);
+      nn = sqrt(block_sum<kJacobiThreads>(nn, S.red));
+      if (nn > 1e-3) {
+        for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] /= nn;
+        __syncthreads();
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  // Q[k][i] = sum_j U[k][j] V[i][j]
+  double* Qb = Q + b * pp;
+  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+    const int k = static_cast<int>(e / p), i = static_cast<int>(e % p);
+    double acc = 0.0;
+    for (int j = 0; j < p; ++j)
+      acc = fma(A[static_cast<int64_t>(j) * p + k], V[static_cast<int64_t>(j) * p + i], acc);
+    Qb[e] = acc;
+  }
+  if (sigma_out)
+    for (int r = threadIdx.x; r < p; r += blockDim.x) sigma_out[b * p + r] = sig[ord[r]];
+  __syncthreads();
+  const double d = defect_of(Qb, p, S.red);
+  if (threadIdx.x == 0 && status) {
+    status[b] = sweeps < 0 ? SBO_ST_NOCONV : (!(d <= 1e-8) ? SBO_ST_DEFECT : SBO_ST_OK);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kJacobiThreads) k_init_block(
+    const double* __restrict__ G, int p, int64_t ncols, const double* __restrict__ draws,
+    int ndraws, double* Q, int32_t* rank_out, int32_t* status, double* ws, int use_smem) {
+  const int64_t pp = static_cast<int64_t>(p) * p;
+  __shared__ JacobiSmem S;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  double *A, *V, *lam, *U;
+  int* ord;
+  double* base = use_smem ? reinterpret_cast<double*>(dyn) : ws;
+  A = base;
+  V = A + pp;
+  U = V + pp;
+  lam = U + pp;
+  ord = reinterpret_cast<int*>(lam + p);
+  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+    const int r = static_cast<int>(e / p), c = static_cast<int>(e % p);
+    A[static_cast<int64_t>(c) * p + r] = G[e];
+    V[static_cast<int64_t>(c) * p + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int sweeps = jacobi_sweeps(A, V, p, p, &S.flag);
+  column_order(A, p, p, lam, ord, true);  // |G v_j| = lambda_j
+  const double l0 = lam[ord[0]];
+  // kept directions: sqrt(l) > 1e-12 sqrt(l0) and above the Gram floor; at most ncols
+  if (threadIdx.x == 0) {
+    int r = 0;
+    if (l0 > 0.0) {
+      const int cap = static_cast<int>(ncols < p ? ncols : p);
+      while (r < cap) {
+        const double l = lam[ord[r]];
+        if (!(sqrt(l) > 1e-12 * sqrt(l0)) || !(l > 64.0 * DBL_EPSILON * l0)) break;
+        ++r;
+      }
+    }
+    S.count = r;
+  }
+  __syncthreads();
+  const int rank = S.count;
+  // copy kept eigenvectors (descending) into U with canonical signs
+  for (int c = threadIdx.x; c < rank; c += blockDim.x) {
+    const double* v = V + static_cast<int64_t>(ord[c]) * p;
+    int piv = 0;
+    double best = -1.0;
+    for (int r = 0; r < p; ++r)
+      if (fabs(v[r]) > best) {
+        best = fabs(v[r]);
+        piv = r;
+      }
+    const double sgn = v[piv] < 0.0 ? -1.0 : 1.0;
+    double* u = U + static_cast<int64_t>(c) * p;
+    for (int r = 0; r < p; ++r) u[r] = sgn * v[r];
+  }
+  __syncthreads();
+  // seeded completion: twice-projected Gram–Schmidt on the draws, in order
+  int have = rank, d = 0;
+  bool ran_out = false;
+  while (have < p) {
+    if (d >= ndraws) {
+      ran_out = true;
+      break;
+    }
+    double* u = U + static_cast<int64_t>(have) * p;
+    for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] = draws[static_cast<int64_t>(d) * p + r];
+    __syncthreads();
+    ++d;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int l = 0; l < have; ++l) {
+        const double* w = U + static_cast<int64_t>(l) * p;
+        double dd = 0.0;
+        for (int r = threadIdx.x; r < p; r += blockDim.x) dd = fma(w[r], u[r], dd);
+        dd = block_sum<kJacobiThreads>(dd, S.red);
+        for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] -= dd * w[r];
+        __syncthreads();
+      }
+    }
+    double nn = 0.0;
+    for (int r = threadIdx.x; r < p; r += blockDim.x) nn = fma(u[r], u[r], nn);
+    nn = sqrt(block_sum<kJacobiThreads>(nn, S.red));
+    if (nn < 1e-8) continue;
+    for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] /= nn;
+    __syncthreads();
+    ++have;
+  }
+  // Q[k][i] = U column i, row k
+  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+    const int k = static_cast<int>(e / p), i = static_cast<int>(e % p);
+    Q[e] = U[static_cast<int64_t>(i) * p + k];
+  }
+  __syncthreads();
+  const double df = defect_of(Q, p, S.red);
+  if (threadIdx.x == 0) {
+    if (rank_out) {
+      rank_out[0] = rank;
+      rank_out[1] = d;  // completion draws consumed
+    }
+    if (status)
+      *status = (sweeps < 0 || ran_out) ? SBO_ST_NOCONV : (!(df <= 1e-8) ? SBO_ST_DEFECT : SBO_ST_OK);
+  }
+}
+
+}  // namespace sbo
+
+using namespace sbo;
+
+namespace {
+size_t polar_smem_bytes(int p) {
+  const size_t pp = static_cast<size_t>(p) * p;
+  return sizeof(double) * (2 * pp + 2 * p);
+}
+size_t init_smem_bytes(int p) {
+  const size_t pp = static_cast<size_t>(p) * p;
+  return sizeof(double) * (3 * pp + 2 * p);
+}
+constexpr size_t kSmemBudget = 200 * 1024;
+}  // namespace
+
+extern "C" size_t sbo_polar_workspace_bytes(int K, int p) {
+  return static_cast<size_t>(K) * polar_smem_bytes(p) + 64;
+}
+
+extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, double* Q,
+                         double* sigma, int32_t* status, void* ws, size_t ws_bytes,
+                         void* stream) {
+  if (K < 1 || p < 1 || p > kPMax) return fail(SBO_EINVAL, "bad polar shape");
+  const bool smem = polar_smem_bytes(p) <= kSmemBudget;
+  if (!smem && ws_bytes < sbo_polar_workspace_bytes(K, p))
+    return fail(SBO_EINVAL, "polar workspace too small");
+  const size_t dyn = smem ? polar_smem_bytes(p) : 0;
+  cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+  k_polar<<<K, kJacobiThreads, dyn, as_stream(stream)>>>(P, p, counts, Q, sigma, status,
+                                                         static_cast<double*>(ws), smem ? 1 : 0);
+  return check_launch("k_polar");
+}
+
+extern "C" size_t sbo_init_workspace_bytes(int p) { return init_smem_bytes(p) + 64; }
+
+extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const double* draws,
+                              int ndraws, double* Q, int32_t* rank, int32_t* status, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (p < 1 || p > kPMax) return fail(SBO_EINVAL, "bad init shape");
+  const bool smem = init_smem_bytes(p) <= kSmemBudget;
+  if (!smem && ws_bytes < sbo_init_workspace_bytes(p))
+    return fail(SBO_EINVAL, "init workspace too small");
+  const size_t dyn = smem ? init_smem_bytes(p) : 0;
+  cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(dyn));
+  k_init_block<<<1, kJacobiThreads, dyn, as_stream(stream)>>>(
+      G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), smem ? 1 : 0);
+  return check_launch("k_init_block");
+}
+
+// ---------------------------------------------------------------------------
+// Thin SVD of a rows x cols matrix (rows >= cols), linalg.py:40-65: one-sided
+// Jacobi on the columns, singular values descending (index tie-break), U
+// columns with their largest-|entry| nonnegative (linalg.py:32-37), V matched.
+// Directions with sigma <= 64 eps sigma_max get a deterministic orthonormal
+// completion (the reference accepts whatever orthogonal factor its SVD yields
+// for them, SPEC linalg-core design decisions).  Global-memory workspace.
+// Outputs are row-major: U[rows][cols], V[cols][cols], S[cols].
+__global__ void __launch_bounds__(kJacobiThreads) k_svd(const double* __restrict__ M, int rows,
+                                                        int cols, double* U, double* S,
+                                                        double* Vout, int32_t* status,
+                                                        double* ws) {
+  __shared__ JacobiSmem Sm;
+  const int64_t rc = static_cast<int64_t>(rows) * cols;
+  double* A = ws;                 // cols columns of length rows
+  double* V = A + rc;             // cols x cols, column-major
+  double* sig = V + static_cast<int64_t>(cols) * cols;
+  int* ord = reinterpret_cast<int*>(sig + cols);
+  for (int64_t e = threadIdx.x; e < rc; e += blockDim.x) {
+    const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
+    A[static_cast<int64_t>(c) * rows + r] = M[e];
+  }
+  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(cols) * cols; e += blockDim.x)
+    V[e] = (e / cols == e % cols) ? 1.0 : 0.0;
+  __syncthreads();
+  const int sweeps = jacobi_sweeps(A, V, rows, cols, &Sm.flag);
+  column_order(A, rows, cols, sig, ord, true);
+  const double smax = sig[ord[0]];
+  const double null_tol = smax * 64.0 * DBL_EPSILON;
+  for (int64_t e = threadIdx.x; e < rc; e += blockDim.x) {
+    const int j = static_cast<int>(e / rows);
+    if (sig[j] > null_tol) A[e] /= sig[j];
+  }
+  __syncthreads();
+  for (int rnk = 0; rnk < cols; ++rnk) {
+    const int j = ord[rnk];
+    if (sig[j] > null_tol) continue;
+    double* u = A + static_cast<int64_t>(j) * rows;
+    for (int cand = 0; cand < rows; ++cand) {
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) u[r] = (r == cand) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int l = 0; l < cols; ++l) {
+          const int jl = ord[l];
+          if (jl == j || (sig[jl] <= null_tol && l > rnk)) continue;
+          const double* w = A + static_cast<int64_t>(jl) * rows;
+          double d = 0.0;
+          for (int r = threadIdx.x; r < rows; r += blockDim.x) d = fma(w[r], u[r], d);
+          d = block_sum<kJacobiThreads>(d, Sm.red);
+          for (int r = threadIdx.x; r < rows; r += blockDim.x) u[r] -= d * w[r];
+          __syncthreads();
+        }
+      }
+      double nn = 0.0;
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) nn = fma(u[r], u[r], nn);
+      nn = sqrt(block_sum<kJacobiThreads>(nn, Sm.red));
+      if (nn > 1e-3) {
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) u[r] /= nn;
+        __syncthreads();
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  // canonical signs, sorted output
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const int j = ord[c];
+    const double* u = A + static_cast<int64_t>(j) * rows;
+    int piv = 0;
+    double best = -1.0;
+    for (int r = 0; r < rows; ++r)
+      if (fabs(u[r]) > best) {
+        best = fabs(u[r]);
+        piv = r;
+      }
+    const double sgn = u[piv] < 0.0 ? -1.0 : 1.0;
+    for (int r = 0; r < rows; ++r) U[static_cast<int64_t>(r) * cols + c] = sgn * u[r];
+    const double* v = V + static_cast<int64_t>(j) * cols;
+    for (int r = 0; r < cols; ++r) Vout[static_cast<int64_t>(r) * cols + c] = sgn * v[r];
+    S[c] = sig[j];
+  }
+  if (threadIdx.x == 0 && status) *status = sweeps < 0 ? SBO_ST_NOCONV : SBO_ST_OK;
+}
+
+extern "C" size_t sbo_svd_workspace_bytes(int rows, int cols) {
+  return sizeof(double) * (static_cast<size_t>(rows) * cols + static_cast<size_t>(cols) * cols +
+                           2 * static_cast<size_t>(cols)) + 64;
+}
+
+extern "C" int sbo_svd(const double* M, int rows, int cols, double* U, double* S, double* V,
+                       int32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  if (rows < 1 || cols < 1 || cols > rows) return fail(SBO_EINVAL, "sbo_svd needs rows >= cols >= 1");
+  if (ws_bytes < sbo_svd_workspace_bytes(rows, cols)) return fail(SBO_EINVAL, "svd workspace too small");
+  k_svd<<<1, kJacobiThreads, 0, as_stream(stream)>>>(M, rows, cols, U, S, V, status,
+                                                     static_cast<double*>(ws));
+  return check_launch("k_svd");
+}

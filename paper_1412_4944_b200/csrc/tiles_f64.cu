@@ -1,0 +1,564 @@
+// Float64 tile kernels: projection onto orthonormal blocks, exact hard-threshold
+// selection, energy/argmax, own-block coding and sparse outer products.
+//
+// These are the exact (float64, CUDA-core) implementations of the reference's
+// represent / select_top / sparse_outer (sbo.py:138-220, onb.py:58-76, 127-134).
+// They serve every signal dimension p <= 256 and every s0, and they are the
+// certification path of the tensor-core kernels (tc_represent.cu).
+//
+// Tile geometry: a CTA of 256 threads owns 64 signals.  C = Y_tile . Q_b is
+// built in 64x64 chunks with a 4x4 register tile per thread (y and q staged in
+// shared memory as float64), then each warp ranks its signals' coefficients:
+// coefficient i is kept iff fewer than k coefficients beat it under the key
+// (|c| descending, index ascending) — the stable-argsort rule of onb.py:73.
+#include "common.cuh"
+
+namespace sbo {
+
+constexpr int kSyLd = kTile + 2;  // float64 row stride of the staged y chunk (16B aligned rows)
+
+struct TileLayout {
+  int p, ldc;
+  size_t c_off, y_off, q_off, rows_off, misc_off, bytes;
+  __host__ __device__ explicit TileLayout(int p_) : p(p_) {
+    ldc = p + 1;
+    c_off = 0;
+    y_off = c_off + sizeof(double) * kTile * ldc;
+    y_off = (y_off + 15) & ~size_t(15);
+    q_off = y_off + sizeof(double) * 64 * kSyLd;
+    rows_off = q_off + sizeof(double) * 64 * 64;
+    misc_off = rows_off + sizeof(int64_t) * kTile;
+    bytes = misc_off + sizeof(double) * kTile * 3 + sizeof(int) * kTile + 64;
+  }
+};
+
+// C[s][i] = sum_k y[rows[s]][k] * Q[k][i]  (float64 FMA chain over k ascending)
+template <typename TY>
+__device__ void project_tile(const TY* __restrict__ y, int p, const int64_t* rows,
+                             const double* __restrict__ q, double* C, int ldc, double* sY,
+                             double* sQ) {
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int ic = 0; ic < p; ic += 64) {
+    const int in = min(64, p - ic);
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int kc = 0; kc < p; kc += 64) {
+      const int kn = min(64, p - kc);
+      __syncthreads();
+      for (int e = tid; e < kTile * 64; e += kThreads) {
+        const int s = e >> 6, kk = e & 63;
+        const int64_t r = rows[s];
+        double v = 0.0;
+        if (r >= 0 && kk < kn) v = static_cast<double>(__ldg(y + r * p + kc + kk));
+        sY[kk * kSyLd + s] = v;
+      }
+      for (int e = tid; e < 64 * 64; e += kThreads) {
+        const int kk = e >> 6, ii = e & 63;
+        sQ[e] = (kk < kn && ii < in) ? __ldg(q + static_cast<int64_t>(kc + kk) * p + ic + ii) : 0.0;
+      }
+      __syncthreads();
+      for (int kk = 0; kk < kn; ++kk) {
+        const double2 y01 = *reinterpret_cast<const double2*>(sY + kk * kSyLd + 4 * ty);
+        const double2 y23 = *reinterpret_cast<const double2*>(sY + kk * kSyLd + 4 * ty + 2);
+        const double2 q01 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx);
+        const double2 q23 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx + 2);
+        const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
+        const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(yv[a], qv[b], acc[a][b]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (4 * tx + b < in) C[(4 * ty + a) * ldc + ic + 4 * tx + b] = acc[a][b];
+  }
+  __syncthreads();
+}
+
+// Exact top-k of one coefficient row, warp-cooperative.  Lane l owns the
+// coefficients i = l + 32 t.  Returns the selected mask bit t in `sel`.
+struct RowPick {
+  unsigned sel;     // bit t: coefficient lane+32t kept
+  double score;     // warp-reduced: sum of kept c^2 (kind 0) or |c| (kind 1)
+  double kept_sq;   // warp-reduced: sum of kept c^2
+};
+
+__device__ RowPick pick_row(const double* Cs, int p, int k, int kind) {
+  const int lane = threadIdx.x & 31;
+  const int T = (p + 31) >> 5;
+  double a[8];
+  int rank[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int i = lane + 32 * t;
+    a[t] = (t < T && i < p) ? fabs(Cs[i]) : -1.0;
+    rank[t] = 0;
+  }
+  for (int j = 0; j < p; ++j) {
+    const double cj = fabs(Cs[j]);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (t < T) {
+        const int i = lane + 32 * t;
+        rank[t] += (cj > a[t]) || (cj == a[t] && j < i);
+      }
+    }
+  }
+  RowPick r;
+  r.sel = 0u;
+  double sc = 0.0, sq = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int i = lane + 32 * t;
+    if (t < T && i < p && rank[t] < k) {
+      r.sel |= 1u << t;
+      const double c = Cs[i];
+      sq = fma(c, c, sq);
+      sc += (kind == SBO_KIND_SQUARED_SUM) ? c * c : fabs(c);
+    }
+  }
+  r.score = warp_sum(kind == SBO_KIND_SQUARED_SUM ? sq : sc);
+  r.kept_sq = warp_sum(sq);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// energy pass (sbo.py:177-194), fresh or incremental
+// ---------------------------------------------------------------------------
+template <typename TY>
+__global__ void __launch_bounds__(kThreads) k_energy_f64(
+    const TY* __restrict__ y, int64_t m, int p, const double* __restrict__ blocks, int b0,
+    int b1, int k, int kind, int accumulate, int32_t* best, double* score, double* kept_sq,
+    double* norm_sq) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const TileLayout L(p);
+  double* C = reinterpret_cast<double*>(smem + L.c_off);
+  double* sY = reinterpret_cast<double*>(smem + L.y_off);
+  double* sQ = reinterpret_cast<double*>(smem + L.q_off);
+  int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
+  double* bscore = reinterpret_cast<double*>(smem + L.misc_off);
+  double* bkept = bscore + kTile;
+  double* bnorm = bkept + kTile;
+  int* bbest = reinterpret_cast<int*>(bnorm + kTile);
+
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < kTile) {
+    const int64_t j = base + threadIdx.x;
+    rows[threadIdx.x] = j < m ? j : -1;
+    if (accumulate && j < m) {
+      bbest[threadIdx.x] = best[j];
+      bscore[threadIdx.x] = score[j];
+      bkept[threadIdx.x] = kept_sq[j];
+    } else {
+      bbest[threadIdx.x] = -1;
+      bscore[threadIdx.x] = -1.0;
+      bkept[threadIdx.x] = 0.0;
+    }
+  }
+  __syncthreads();
+  for (int b = b0; b < b1; ++b) {
+    project_tile(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
+    for (int s = warp; s < kTile; s += kThreads / 32) {
+      if (rows[s] < 0) continue;
+      const RowPick r = pick_row(C + s * L.ldc, p, k, kind);
+      if (lane == 0 && r.score > bscore[s]) {  // strict: first maximum wins (sbo.py:191)
+        bscore[s] = r.score;
+        bkept[s] = r.kept_sq;
+        bbest[s] = b;
+      }
+    }
+    __syncthreads();
+  }
+  // ||y||^2 in float64
+  for (int s = warp; s < kTile; s += kThreads / 32) {
+    const int64_t j = rows[s];
+    if (j < 0) continue;
+    double acc = 0.0;
+    for (int kk = lane; kk < p; kk += 32) {
+      const double v = y[j * p + kk];
+      acc = fma(v, v, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) bnorm[s] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < kTile && rows[threadIdx.x] >= 0) {
+    const int64_t j = rows[threadIdx.x];
+    best[j] = bbest[threadIdx.x];
+    score[j] = bscore[threadIdx.x];
+    kept_sq[j] = bkept[threadIdx.x];
+    if (norm_sq) norm_sq[j] = bnorm[threadIdx.x];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// own-block coding over segments (sbo.py:196-211, onb.py:170)
+// ---------------------------------------------------------------------------
+template <typename TY>
+__global__ void __launch_bounds__(kThreads) k_code_f64(
+    const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
+    const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
+    const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
+    const double* __restrict__ blocks, int block_override, int k, int kind, int out_by_signal,
+    int64_t ld, int16_t* idx, double* val, double* energy, double* kept_sq) {
+  if (static_cast<int>(blockIdx.x) >= *nseg) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const TileLayout L(p);
+  double* C = reinterpret_cast<double*>(smem + L.c_off);
+  double* sY = reinterpret_cast<double*>(smem + L.y_off);
+  double* sQ = reinterpret_cast<double*>(smem + L.q_off);
+  int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
+
+  const int seg = blockIdx.x;
+  const int b = block_override >= 0 ? block_override : seg_block[seg];
+  const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+  const double* q = blocks + static_cast<int64_t>(b) * p * p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
+    __syncthreads();
+    if (threadIdx.x < kTile) {
+      const int64_t t = t0 + threadIdx.x;
+      rows[threadIdx.x] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+    }
+    __syncthreads();
+    project_tile(y, p, rows, q, C, L.ldc, sY, sQ);
+    for (int s = warp; s < kTile; s += kThreads / 32) {
+      if (rows[s] < 0) continue;
+      const double* Cs = C + s * L.ldc;
+      const RowPick r = pick_row(Cs, p, k, kind);
+      const int64_t col = out_by_signal ? rows[s] : (t0 + s);
+      int pos = 0;
+      const int T = (p + 31) >> 5;
+      for (int t = 0; t < T; ++t) {
+        const bool on = (r.sel >> t) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (on) {
+          const int at = pos + __popc(bal & lt);
+          idx[at * ld + col] = static_cast<int16_t>(lane + 32 * t);
+          val[at * ld + col] = Cs[lane + 32 * t];
+        }
+        pos += __popc(bal);
+      }
+      if (lane == 0) {
+        if (energy) energy[col] = r.score;
+        if (kept_sq) kept_sq[col] = r.kept_sq;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sparse outer products P = Y X^T per segment (onb.py:127-134) and the Gram
+// matrix of a member list (X = Y).  The code block is densified per 64-column
+// chunk in shared memory; P is accumulated in registers (4x4 per thread) in
+// signal order, so partials are deterministic.
+// ---------------------------------------------------------------------------
+struct OuterLayout {
+  size_t yt_off, x_off, rows_off, bytes;
+  __host__ __device__ OuterLayout() {
+    yt_off = 0;
+    x_off = yt_off + sizeof(double) * kTile * kSyLd;
+    rows_off = x_off + sizeof(double) * kTile * kSyLd;
+    bytes = rows_off + sizeof(int64_t) * kTile;
+  }
+};
+
+template <typename TY>
+__global__ void __launch_bounds__(kThreads) k_outer_f64(
+    const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
+    const int64_t* __restrict__ seg_lo, const int64_t* __restrict__ seg_hi,
+    const int32_t* __restrict__ nseg, int k, int64_t ld, const int16_t* __restrict__ idx,
+    const double* __restrict__ val, int dense_self, double* partial) {
+  if (static_cast<int>(blockIdx.x) >= *nseg) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const OuterLayout L;
+  double* sYt = reinterpret_cast<double*>(smem + L.yt_off);  // [s][kk]
+  double* sX = reinterpret_cast<double*>(smem + L.x_off);    // [s][ii]
+  int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int seg = blockIdx.x;
+  const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+  double* out = partial + static_cast<int64_t>(seg) * p * p;
+
+  for (int kc = 0; kc < p; kc += 64) {
+    const int kn = min(64, p - kc);
+    for (int ic = 0; ic < p; ic += 64) {
+      const int in = min(64, p - ic);
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
+        __syncthreads();
+        if (tid < kTile) {
+          const int64_t t = t0 + tid;
+          rows[tid] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+        }
+        __syncthreads();
+        for (int e = tid; e < kTile * 64; e += kThreads) {
+          const int s = e >> 6, kk = e & 63;
+          const int64_t r = rows[s];
+          double v = 0.0, x = 0.0;
+          if (r >= 0) {
+            if (kk < kn) v = static_cast<double>(__ldg(y + r * p + kc + kk));
+            if (dense_self && kk < in) x = static_cast<double>(__ldg(y + r * p + ic + kk));
+          }
+          sYt[s * kSyLd + kk] = v;
+          sX[s * kSyLd + kk] = x;
+        }
+        if (!dense_self) {
+          __syncthreads();
+          for (int e = tid; e < kTile * k; e += kThreads) {
+            const int s = e / k, rr = e % k;
+            if (rows[s] < 0) continue;
+            const int64_t col = t0 + s;
+            const int i = idx[rr * ld + col];
+            if (i >= ic && i < ic + in) sX[s * kSyLd + (i - ic)] = val[rr * ld + col];
+          }
+        }
+        __syncthreads();
+        const int ns = static_cast<int>(min64(kTile, hi - t0));
+        for (int s = 0; s < ns; ++s) {
+          const double2 y01 = *reinterpret_cast<const double2*>(sYt + s * kSyLd + 4 * ty);
+          const double2 y23 = *reinterpret_cast<const double2*>(sYt + s * kSyLd + 4 * ty + 2);
+          const double2 x01 = *reinterpret_cast<const double2*>(sX + s * kSyLd + 4 * tx);
+          const double2 x23 = *reinterpret_cast<const double2*>(sX + s * kSyLd + 4 * tx + 2);
+          const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
+          const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(yv[a], xv[b], acc[a][b]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (4 * ty + a < kn && 4 * tx + b < in)
+            out[static_cast<int64_t>(kc + 4 * ty + a) * p + ic + 4 * tx + b] = acc[a][b];
+    }
+  }
+}
+
+// P_b = sum of block b's segment partials, in segment order
+__global__ void k_reduce_segments(const double* __restrict__ partial,
+                                  const int32_t* __restrict__ seg_block,
+                                  const int32_t* __restrict__ nseg, int K, int p, double* P) {
+  const int b = blockIdx.y;
+  const int64_t pp = static_cast<int64_t>(p) * p;
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= pp) return;
+  const int n = *nseg;
+  double acc = 0.0;
+  bool any = false;
+  for (int s = 0; s < n; ++s) {
+    if (seg_block ? seg_block[s] == b : b == 0) {
+      acc += partial[s * pp + e];
+      any = true;
+    }
+  }
+  P[b * pp + e] = any ? acc : 0.0;
+}
+
+// Gram partials over chunks of a member list, then the ordered reduction
+__global__ void k_chunk_segments(int64_t w, int chunk, int64_t* lo, int64_t* hi, int32_t* nseg) {
+  const int64_t n = ceil_div(w, chunk);
+  for (int64_t s = threadIdx.x; s < n; s += blockDim.x) {
+    lo[s] = s * chunk;
+    hi[s] = min64(w, (s + 1) * chunk);
+  }
+  if (threadIdx.x == 0) *nseg = static_cast<int32_t>(n);
+}
+
+}  // namespace sbo
+
+using namespace sbo;
+
+namespace {
+template <typename TY>
+int energy_impl(const void* yv, int64_t m, int p, const double* blocks, int b0, int b1, int k,
+                int kind, int accumulate, int32_t* best, double* score, double* kept_sq,
+                double* norm_sq, cudaStream_t st) {
+  const TileLayout L(p);
+  cudaFuncSetAttribute(k_energy_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(L.bytes));
+  k_energy_f64<TY><<<static_cast<unsigned>(ceil_div(m, kTile)), kThreads, L.bytes, st>>>(
+      static_cast<const TY*>(yv), m, p, blocks, b0, b1, k, kind, accumulate, best, score,
+      kept_sq, norm_sq);
+  return check_launch("k_energy_f64");
+}
+
+template <typename TY>
+int code_impl(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
+              const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
+              int64_t max_seg, const double* blocks, int block_override, int k, int kind,
+              int out_by_signal, int64_t ld, int16_t* idx, double* val, double* energy,
+              double* kept_sq, cudaStream_t st) {
+  const TileLayout L(p);
+  cudaFuncSetAttribute(k_code_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(L.bytes));
+  k_code_f64<TY><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
+      static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
+      block_override, k, kind, out_by_signal, ld, idx, val, energy, kept_sq);
+  return check_launch("k_code_f64");
+}
+
+template <typename TY>
+int outer_impl(const void* yv, int p, const int32_t* order, const int64_t* seg_lo,
+               const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg, int k, int64_t ld,
+               const int16_t* idx, const double* val, int dense_self, double* partial,
+               cudaStream_t st) {
+  const OuterLayout L;
+  cudaFuncSetAttribute(k_outer_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(L.bytes));
+  k_outer_f64<TY><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
+      static_cast<const TY*>(yv), p, order, seg_lo, seg_hi, nseg, k, ld, idx, val, dense_self,
+      partial);
+  return check_launch("k_outer_f64");
+}
+
+int check_common(int dtype, int p, int s0) {
+  if (dtype != SBO_F32 && dtype != SBO_F64) return fail(SBO_EINVAL, "dtype must be SBO_F32 or SBO_F64");
+  if (p < 1 || p > kPMax) return fail(SBO_EINVAL, "p must be in [1, 256]");
+  if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
+  return SBO_OK;
+}
+}  // namespace
+
+extern "C" int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* blocks,
+                               int b0, int b1, int s0, int kind, int accumulate, int32_t* best,
+                               double* score, double* kept_sq, double* norm_sq, void* stream) {
+  if (int rc = check_common(dtype, p, s0)) return rc;
+  if (b0 < 0 || b1 < b0 || (!accumulate && b0 != 0))
+    return fail(SBO_EINVAL, "bad block range for the energy pass");
+  if (m == 0 || b1 == b0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? energy_impl<float>(y, m, p, blocks, b0, b1, k, kind, accumulate, best, score,
+                                  kept_sq, norm_sq, as_stream(stream))
+             : energy_impl<double>(y, m, p, blocks, b0, b1, k, kind, accumulate, best, score,
+                                   kept_sq, norm_sq, as_stream(stream));
+}
+
+extern "C" int sbo_code_segments(const void* y, int dtype, int p, const int32_t* order,
+                                 const int32_t* seg_block, const int64_t* seg_lo,
+                                 const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                                 const double* blocks, int block_override, int s0, int kind,
+                                 int out_by_signal, int64_t ld, int16_t* idx, double* val,
+                                 double* energy, double* kept_sq, void* stream) {
+  if (int rc = check_common(dtype, p, s0)) return rc;
+  if (max_seg <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? code_impl<float>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
+                                block_override, k, kind, out_by_signal, ld, idx, val, energy,
+                                kept_sq, as_stream(stream))
+             : code_impl<double>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
+                                 block_override, k, kind, out_by_signal, ld, idx, val, energy,
+                                 kept_sq, as_stream(stream));
+}
+
+extern "C" int sbo_outer_segments(const void* y, int dtype, int p, const int32_t* order,
+                                  const int64_t* seg_lo, const int64_t* seg_hi,
+                                  const int32_t* nseg, int64_t max_seg, int s0, int64_t ld,
+                                  const int16_t* idx, const double* val, double* partial,
+                                  void* stream) {
+  if (int rc = check_common(dtype, p, s0)) return rc;
+  if (max_seg <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? outer_impl<float>(y, p, order, seg_lo, seg_hi, nseg, max_seg, k, ld, idx, val, 0,
+                                 partial, as_stream(stream))
+             : outer_impl<double>(y, p, order, seg_lo, seg_hi, nseg, max_seg, k, ld, idx, val,
+                                  0, partial, as_stream(stream));
+}
+
+extern "C" int sbo_reduce_segments(const double* partial, const int32_t* seg_block,
+                                   const int32_t* nseg, int64_t max_seg, int K, int p,
+                                   double* P, void* stream) {
+  if (K < 1 || p < 1) return fail(SBO_EINVAL, "bad reduce shape");
+  (void)max_seg;
+  const int64_t pp = static_cast<int64_t>(p) * p;
+  dim3 grid(static_cast<unsigned>(ceil_div(pp, 256)), static_cast<unsigned>(K));
+  k_reduce_segments<<<grid, 256, 0, as_stream(stream)>>>(partial, seg_block, nseg, K, p, P);
+  return check_launch("k_reduce_segments");
+}
+
+extern "C" size_t sbo_gram_workspace_bytes(int64_t w, int chunk, int p) {
+  const int64_t n = ceil_div(w > 0 ? w : 1, chunk > 0 ? chunk : 1);
+  return sizeof(double) * n * p * p + sizeof(int64_t) * 2 * n + 64;
+}
+
+extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members, int64_t w,
+                        int chunk, double* G, void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = check_common(dtype, p, 1)) return rc;
+  if (chunk < kTile || chunk % kTile) return fail(SBO_EINVAL, "chunk must be a multiple of 64");
+  if (ws_bytes < sbo_gram_workspace_bytes(w, chunk, p))
+    return fail(SBO_EINVAL, "gram workspace too small");
+  cudaStream_t st = as_stream(stream);
+  if (w <= 0) {
+    SBO_CHECK_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * p * p, st));
+    return SBO_OK;
+  }
+  const int64_t n = ceil_div(w, chunk);
+  double* partial = static_cast<double*>(ws);
+  int64_t* lo = reinterpret_cast<int64_t*>(partial + n * p * p);
+  int64_t* hi = lo + n;
+  int32_t* ns = reinterpret_cast<int32_t*>(hi + n);
+  k_chunk_segments<<<1, 256, 0, st>>>(w, chunk, lo, hi, ns);
+  int rc = dtype == SBO_F32 ? outer_impl<float>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
+                                                nullptr, 1, partial, st)
+                            : outer_impl<double>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
+                                                 nullptr, 1, partial, st);
+  if (rc) return rc;
+  const int64_t pp = static_cast<int64_t>(p) * p;
+  k_reduce_segments<<<dim3(static_cast<unsigned>(ceil_div(pp, 256)), 1), 256, 0, st>>>(
+      partial, nullptr, ns, 1, p, G);
+  return check_launch("k_reduce_segments(gram)");
+}
+
+// select_top on explicit float64 coefficients (onb.py:58-76): coefficient
+// vectors are rows of `coeffs` (t x p); warp per vector.
+__global__ void k_select_rows(const double* __restrict__ coeffs, int64_t t, int p, int k,
+                              int64_t ld, int16_t* idx, double* val) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
+  if (j >= t) return;
+  const double* Cs = coeffs + j * p;
+  const RowPick r = pick_row(Cs, p, k, SBO_KIND_SQUARED_SUM);
+  const unsigned lt = (1u << lane) - 1u;
+  int pos = 0;
+  const int T = (p + 31) >> 5;
+  for (int q = 0; q < T; ++q) {
+    const bool on = (r.sel >> q) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (on) {
+      const int at = pos + __popc(bal & lt);
+      idx[at * ld + j] = static_cast<int16_t>(lane + 32 * q);
+      val[at * ld + j] = Cs[lane + 32 * q];
+    }
+    pos += __popc(bal);
+  }
+}
+
+extern "C" int sbo_select_top(const double* coeffs, int64_t t, int p, int s0, int64_t ld,
+                              int16_t* idx, double* val, void* stream) {
+  if (p < 1 || p > kPMax) return fail(SBO_EINVAL, "p must be in [1, 256]");
+  if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
+  if (t == 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  k_select_rows<<<static_cast<unsigned>(ceil_div(t, 8)), 256, 0, as_stream(stream)>>>(
+      coeffs, t, p, k, ld, idx, val);
+  return check_launch("k_select_rows");
+}

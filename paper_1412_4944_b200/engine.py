@@ -1,0 +1,414 @@
+"""Device-resident SBO engine: the host orchestration of one iteration.
+
+Everything numeric runs in the sm_100a library through the C ABI
+(include/sbo_b200.h); this module owns device buffers (allocated with torch,
+which is only plumbing here: memory, streams, NCCL), sequences the kernels of
+one ``sbo_train`` loop body (sbo.py:352-397) without host round-trips, and
+performs the cross-rank reductions when signals are sharded over GPUs.
+
+Per iteration (K-1 blocks entering, K leaving):
+  worst set      sbo_worst_set (radix select, ties -> low index)   sbo.py:353
+  new block      sbo_gram -> [allreduce] -> sbo_init_block          sbo.py:354-356
+                 R x (code -> outer -> reduce -> [allreduce] -> polar)
+  represent #1   sbo_energy_pass(accumulate, new block only)        sbo.py:361
+  group          sbo_group (stable counting sort + segment table)  sbo.py:367
+  retrain        R x (code -> outer -> reduce -> [allreduce] -> polar) sbo.py:369-385
+  represent #2   sbo_energy_pass(all blocks) + sbo_residual         sbo.py:389-394
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+SEG_LEN = 1024        # signals per segment of the per-block kernels
+GRAM_CHUNK = 2048     # members per Gram partial
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class Comm:
+    """Cross-rank reductions; the single-GPU instance is the identity."""
+
+    world = 1
+    rank = 0
+
+    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+        return t
+
+    def allgather_int(self, v: int) -> list[int]:
+        return [v]
+
+
+class TorchComm(Comm):
+    """NCCL (or gloo) process group of torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allreduce(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def allgather_int(self, v):
+        t = torch.tensor([v], dtype=torch.int64, device=_comm_device(self.dist))
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+
+def _comm_device(dist):
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" \
+        else torch.device("cpu")
+
+
+def require_device(index: int | None = None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: the SBO kernels require an sm_100a GPU (B200)")
+    dev = torch.device("cuda", torch.cuda.current_device() if index is None else index)
+    if not L.lib().sbo_device_ok(dev.index):
+        raise RuntimeError(f"device {dev} is not an sm_100 (Blackwell) GPU")
+    return dev
+
+
+class Scratch:
+    """Grow-only named device scratch buffers."""
+
+    def __init__(self, device):
+        self.device, self.buf = device, {}
+
+    def get(self, name: str, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 16)
+        t = self.buf.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self.buf[name] = t
+        return t
+
+
+class Signals:
+    """The signal matrix resident on one device: rows (m, p), float32 or float64.
+
+    The reference's column-major p x m float64 matrix is row-major (m, p) here.
+    float32 storage is used whenever it is exact (every value float32-representable),
+    which is the benchmark's case; otherwise float64 keeps arbitrary inputs exact."""
+
+    def __init__(self, rows: torch.Tensor):
+        assert rows.dim() == 2 and rows.is_cuda and rows.is_contiguous()
+        assert rows.dtype in (torch.float32, torch.float64)
+        self.y = rows
+        self.m, self.p = rows.shape
+        self.code = L.F32 if rows.dtype == torch.float32 else L.F64
+
+    @classmethod
+    def from_reference(cls, y: np.ndarray, device, offset: int = 0, count: int | None = None):
+        """Upload columns [offset, offset+count) of a p x m float64 matrix."""
+        p, m = y.shape
+        count = m - offset if count is None else count
+        block = y[:, offset:offset + count]
+        y32 = block.astype(np.float32)
+        exact = np.array_equal(y32.astype(np.float64), block)
+        host = np.ascontiguousarray((y32 if exact else block).T)
+        return cls(torch.from_numpy(host).to(device))
+
+    @classmethod
+    def from_rows(cls, rows: np.ndarray, device):
+        return cls(torch.from_numpy(np.ascontiguousarray(rows)).to(device))
+
+
+@dataclass
+class Groups:
+    perm: torch.Tensor       # int32 (m,)
+    bounds: torch.Tensor     # int64 (K+1,)
+    seg_block: torch.Tensor  # int32 (max_seg,)
+    seg_lo: torch.Tensor     # int64
+    seg_hi: torch.Tensor     # int64
+    nseg: torch.Tensor       # int32 (1,)
+    max_seg: int
+
+    @property
+    def counts(self):
+        return self.bounds[1:] - self.bounds[:-1]
+
+
+@dataclass
+class State:
+    """Per-signal assignment state after a representation pass."""
+    best: torch.Tensor      # int32 (m,)
+    score: torch.Tensor     # float64 (m,) energy-pass score of the winner
+    kept: torch.Tensor      # float64 (m,) kept sum of squares of the winner
+    norm: torch.Tensor      # float64 (m,) ||y||^2
+    residual: torch.Tensor  # float64 (m,)
+    total: torch.Tensor     # float64 (1,) local sum of residuals
+
+
+@dataclass
+class IterationOut:
+    K: int
+    rmse: float
+    empty_blocks: list = field(default_factory=list)
+    worst: torch.Tensor | None = None
+
+
+class Engine:
+    """One process's device state for a (possibly sharded) SBO problem."""
+
+    def __init__(self, sig: Signals, s0: int, kind: str = "squared-sum", k_cap: int = 64,
+                 comm: Comm | None = None, m_total: int | None = None):
+        self.sig, self.s0 = sig, int(s0)
+        self.kind = L.KIND[kind]
+        self.kind_name = kind
+        self.p, self.m = sig.p, sig.m
+        self.k = min(self.s0, self.p)
+        self.dev = sig.y.device
+        self.comm = comm or Comm()
+        self.m_total = self.m if m_total is None else int(m_total)
+        self.k_cap = int(k_cap)
+        self.blocks = torch.zeros((self.k_cap, self.p, self.p), dtype=torch.float64, device=self.dev)
+        self.K = 0
+        self.scratch = Scratch(self.dev)
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.state = State(torch.zeros(self.m, dtype=torch.int32, device=self.dev),
+                           torch.zeros(self.m, **f64), torch.zeros(self.m, **f64),
+                           torch.zeros(self.m, **f64), torch.zeros(self.m, **f64),
+                           torch.zeros(1, **f64))
+        self.idx = torch.empty((self.k, max(self.m, 1)), dtype=torch.int16, device=self.dev)
+        self.val = torch.empty((self.k, max(self.m, 1)), **f64)
+        self.launches = 0
+
+    # ------------------------------------------------------------------ utils
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _call(self, name, *args):
+        self.launches += 1
+        L.call(name, *args)
+        if L.debug_sync():
+            torch.cuda.synchronize(self.dev)
+
+    def set_blocks(self, blocks: np.ndarray | torch.Tensor):
+        t = torch.as_tensor(np.asarray(blocks) if not torch.is_tensor(blocks) else blocks,
+                            dtype=torch.float64)
+        K = t.shape[0]
+        if K > self.k_cap:
+            grown = torch.zeros((K, self.p, self.p), dtype=torch.float64, device=self.dev)
+            self.blocks, self.k_cap = grown, K
+        self.blocks[:K].copy_(t.to(self.dev))
+        self.K = K
+
+    def ensure_capacity(self, K: int):
+        if K > self.k_cap:
+            grown = torch.zeros((K, self.p, self.p), dtype=torch.float64, device=self.dev)
+            grown[: self.K].copy_(self.blocks[: self.K])
+            self.blocks, self.k_cap = grown, K
+
+    def block_ptr(self, b: int) -> int:
+        return self.blocks.data_ptr() + b * self.p * self.p * 8
+
+    # ------------------------------------------------------ representation
+    def energy(self, b0: int, b1: int, accumulate: bool):
+        s = self.state
+        self._call("sbo_energy_pass", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
+                   self.blocks.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
+                   s.best.data_ptr(), s.score.data_ptr(), s.kept.data_ptr(),
+                   None if accumulate else s.norm.data_ptr(), self.stream)
+
+    def residual(self):
+        s = self.state
+        ws = self.scratch.get("sum", L.size("sbo_sum_workspace_bytes", self.m))
+        self._call("sbo_residual", s.norm.data_ptr(), s.kept.data_ptr(), self.m,
+                   s.residual.data_ptr(), s.total.data_ptr(), ws.data_ptr(), ws.numel(),
+                   self.stream)
+
+    def group(self, K: int) -> Groups:
+        max_seg = L.size("sbo_max_segments", self.m, K, SEG_LEN)
+        d = self.dev
+        g = Groups(torch.empty(max(self.m, 1), dtype=torch.int32, device=d),
+                   torch.empty(K + 1, dtype=torch.int64, device=d),
+                   torch.empty(max_seg, dtype=torch.int32, device=d),
+                   torch.empty(max_seg, dtype=torch.int64, device=d),
+                   torch.empty(max_seg, dtype=torch.int64, device=d),
+                   torch.zeros(1, dtype=torch.int32, device=d), max_seg)
+        ws = self.scratch.get("group", L.size("sbo_group_workspace_bytes", self.m, K))
+        self._call("sbo_group", self.state.best.data_ptr(), self.m, K, SEG_LEN,
+                   g.perm.data_ptr(), g.bounds.data_ptr(), g.seg_block.data_ptr(),
+                   g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(), ws.data_ptr(),
+                   ws.numel(), self.stream)
+        return g
+
+    def list_segments(self, n: int) -> Groups:
+        """Segment table of a single list of n entries (a member list)."""
+        nseg = max(1, math.ceil(n / SEG_LEN)) if n > 0 else 0
+        lo = torch.arange(0, max(n, 1), SEG_LEN, dtype=torch.int64, device=self.dev)[:nseg]
+        hi = torch.clamp(lo + SEG_LEN, max=n)
+        return Groups(None, None, torch.zeros(max(nseg, 1), dtype=torch.int32, device=self.dev),
+                      lo, hi, torch.tensor([nseg], dtype=torch.int32, device=self.dev),
+                      max(nseg, 1))
+
+    def code(self, order, g: Groups, block_override: int, out_by_signal: bool, ld: int,
+             idx, val, energy=None, kept=None):
+        self._call("sbo_code_segments", self.sig.y.data_ptr(), self.sig.code, self.p,
+                   _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
+                   g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, self.blocks.data_ptr(),
+                   block_override, self.s0, self.kind, int(out_by_signal), ld,
+                   idx.data_ptr(), val.data_ptr(), _ptr(energy), _ptr(kept), self.stream)
+
+    # ----------------------------------------------------------- training
+    def train_rounds(self, order, g: Groups, n: int, rounds: int, nblocks: int,
+                     first_block: int, counts, status: torch.Tensor, single: bool):
+        """R rounds of (code, P = Y X^T, allreduce, polar) for `nblocks` blocks.
+
+        single=True: one block (first_block) over a member list of n entries."""
+        p = self.p
+        partial = self.scratch.get("partial", 8 * g.max_seg * p * p)
+        P = self.scratch.get("P", 8 * nblocks * p * p)
+        ld = max(n, 1)
+        idx = self.scratch.get("tr_idx", 2 * self.k * ld).view(torch.int16)
+        val = self.scratch.get("tr_val", 8 * self.k * ld).view(torch.float64)
+        pol_ws = self.scratch.get("polar", L.size("sbo_polar_workspace_bytes", nblocks, p))
+        Pt = P[: 8 * nblocks * p * p].view(torch.float64).view(nblocks, p, p)
+        for r in range(rounds):
+            self.code(order, g, first_block if single else -1, False, ld, idx, val)
+            self._call("sbo_outer_segments", self.sig.y.data_ptr(), self.sig.code, p,
+                       _ptr(order), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
+                       g.nseg.data_ptr(), g.max_seg, self.s0, ld, idx.data_ptr(),
+                       val.data_ptr(), partial.data_ptr(), self.stream)
+            self._call("sbo_reduce_segments", partial.data_ptr(),
+                       None if single else g.seg_block.data_ptr(), g.nseg.data_ptr(),
+                       g.max_seg, nblocks, p, Pt.data_ptr(), self.stream)
+            self.comm.allreduce(Pt)
+            self._call("sbo_polar", Pt.data_ptr(), nblocks, p, _ptr(counts),
+                       self.block_ptr(first_block), None, status[r].data_ptr(),
+                       pol_ws.data_ptr(), pol_ws.numel(), self.stream)
+
+    def gram(self, members, w: int) -> torch.Tensor:
+        G = torch.empty((self.p, self.p), dtype=torch.float64, device=self.dev)
+        ws = self.scratch.get("gram", L.size("sbo_gram_workspace_bytes", w, GRAM_CHUNK, self.p))
+        self._call("sbo_gram", self.sig.y.data_ptr(), self.sig.code, self.p, _ptr(members), w,
+                   GRAM_CHUNK, G.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
+        return G
+
+    def init_block(self, G, ncols: int, draws: np.ndarray, slot: int, status, rank=None):
+        d = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).to(self.dev)
+        ws = self.scratch.get("init", L.size("sbo_init_workspace_bytes", self.p))
+        self._call("sbo_init_block", G.data_ptr(), self.p, ncols, d.data_ptr(), d.shape[0],
+                   self.block_ptr(slot), _ptr(rank), status.data_ptr(), ws.data_ptr(),
+                   ws.numel(), self.stream)
+
+    def worst(self, w: int) -> tuple[torch.Tensor, int]:
+        """Local members of the global worst-w set (ascending signal order)."""
+        res = self.state.residual
+        if self.comm.world == 1:
+            n = min(w, self.m)
+            members = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+            ws = self.scratch.get("worst", L.size("sbo_worst_workspace_bytes", self.m))
+            self._call("sbo_worst_set", res.data_ptr(), self.m, w, members.data_ptr(),
+                       ws.data_ptr(), ws.numel(), self.stream)
+            return members, n
+        return distributed_worst(self, w)
+
+    # ----------------------------------------------------------- iteration
+    def represent_full(self):
+        self.energy(0, self.K, False)
+        self.residual()
+
+    def rmse(self) -> float:
+        tot = self.comm.allreduce(self.state.total.clone())
+        return math.sqrt(max(float(tot.item()), 0.0) / (self.p * self.m_total))
+
+    def iterate(self, w: int, rounds: int, draws: np.ndarray, timer=None) -> IterationOut:
+        """One SBO iteration (sbo.py:352-397) entering with self.K blocks.
+
+        ``timer.mark()`` (optional) is called at the phase boundaries: start, new
+        block trained, represent #1, retrain, represent #2."""
+        mark = timer.mark if timer is not None else (lambda: None)
+        mark()
+        K0 = self.K
+        self.ensure_capacity(K0 + 1)
+        st = torch.zeros((2, rounds + 1, K0 + 1), dtype=torch.int32, device=self.dev)
+        # worst set and the new block (sbo.py:353-357)
+        members, n = self.worst(w)
+        n_total = min(w, self.m_total)
+        G = self.comm.allreduce(self.gram(members, n))
+        self.init_block(G, n_total, draws, K0, st[0, rounds, :1])
+        segs = self.list_segments(n)
+        self.train_rounds(members, segs, n, rounds, 1, K0, None, st[0], single=True)
+        self.K = K0 + 1
+        mark()
+        # represent #1: only the appended block can change a winner (sbo.py:361)
+        self.energy(K0, K0 + 1, True)
+        mark()
+        # group + retrain every block on its signals (sbo.py:367-385)
+        g = self.group(self.K)
+        counts = g.counts
+        if self.comm.world > 1:
+            counts = self.comm.allreduce(counts.clone())
+        self.train_rounds(g.perm, g, self.m, rounds, self.K, 0, counts, st[1], single=False)
+        mark()
+        # represent #2 (sbo.py:389-394)
+        self.represent_full()
+        mark()
+        rmse = self.rmse()
+        stc = st.cpu().numpy()
+        cnt = counts.cpu().numpy()
+        check_status(stc)
+        empty = [b for b in range(self.K) if cnt[b] == 0]
+        return IterationOut(self.K, rmse, empty, members[:n])
+
+
+def check_status(st: np.ndarray):
+    from .linalg import DecompositionError
+    from .onb import NumericalError
+    if (st == L.ST_NOCONV).any():
+        raise DecompositionError("Jacobi SVD did not converge for a block update")
+    if (st == L.ST_DEFECT).any():
+        raise NumericalError("block lost orthonormality: defect > 1e-08")
+
+
+def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int]:
+    """Global worst-w across ranks: radix select with allreduced 256-bin histograms.
+
+    Keys are the float64 bit patterns of residual_sq (order-preserving for >= 0);
+    ties at the threshold go to the lowest GLOBAL signal index, i.e. to lower
+    ranks first (contiguous column shards)."""
+    res = eng.state.residual
+    m_total = eng.m_total
+    need = min(w, m_total)
+    prefix = 0
+    hist = torch.zeros(256, dtype=torch.int64, device=eng.dev)
+    for shift in range(56, -8, -8):
+        hist.zero_()
+        eng._call("sbo_key_histogram", res.data_ptr(), eng.m, prefix, shift, hist.data_ptr(),
+                  eng.stream)
+        h = eng.comm.allreduce(hist).cpu().numpy()
+        cum = 0
+        for d in range(255, -1, -1):
+            if cum + h[d] >= need:
+                break
+            cum += int(h[d])
+        need -= cum
+        prefix |= d << shift
+    # equal-key members: lowest global indices first -> lower ranks first
+    cnt = torch.zeros(2, dtype=torch.int64, device=eng.dev)
+    members = torch.empty(max(eng.m, 1), dtype=torch.int32, device=eng.dev)
+    ws = eng.scratch.get("worst", L.size("sbo_worst_workspace_bytes", eng.m))
+    # first pass: counts only (take 0 equal keys) to learn this rank's equal count
+    eng._call("sbo_worst_collect", res.data_ptr(), eng.m, prefix, 0, members.data_ptr(),
+              cnt.data_ptr(), ws.data_ptr(), ws.numel(), eng.stream)
+    gt, eq = (int(x) for x in cnt.cpu().numpy())
+    eqs = eng.comm.allgather_int(eq)
+    before = sum(eqs[: eng.comm.rank])
+    take = max(0, min(eq, need - before))
+    eng._call("sbo_worst_collect", res.data_ptr(), eng.m, prefix, take, members.data_ptr(),
+              cnt.data_ptr(), ws.data_ptr(), ws.numel(), eng.stream)
+    return members, gt + take
