@@ -179,7 +179,7 @@ def run_reference(a):
 # --------------------------------------------------------------------------- GPU
 KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1,
                     "sbo_outer_segments": 1, "sbo_reduce_segments": 1, "sbo_polar": 1,
-                    "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_residual": 2,
+                    "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_sum": 2,
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2}
 
 
@@ -214,14 +214,14 @@ def run_ours(a):
     torch.cuda.synchronize()
     snap_blocks = eng.blocks.clone()
     st = eng.state
-    snap = [t.clone() for t in (st.best, st.score, st.kept, st.norm, st.residual, st.total)]
+    snap = [t.clone() for t in (st.best, st.score, st.norm, st.residual, st.total)]
     K0 = eng.K
     draws = _block_rng(1, 1, K0).standard_normal((p + 8, p))
     w = max(p, m_total // 16)
 
     def restore():
         eng.blocks.copy_(snap_blocks)
-        for dst, src in zip((st.best, st.score, st.kept, st.norm, st.residual, st.total), snap):
+        for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total), snap):
             dst.copy_(src)
         eng.K = K0
 
@@ -352,7 +352,7 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
     def step():
         eng.sig.y.copy_(host_y, non_blocking=True)
         eng.blocks[:K0].copy_(host_blocks, non_blocking=True)
-        for dst, src in zip((st.best, st.score, st.kept, st.norm, st.residual, st.total),
+        for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total),
                             host_state):
             dst.copy_(src, non_blocking=True)
         eng.K = K0

@@ -60,14 +60,16 @@ int sbo_device_ok(int device);
  * For every signal j < m and block b in [b0, b1): c = Q_b^T y_j, score =
  * sum of the k largest c^2 (kind 0) or |c| (kind 1); the winner is the first
  * maximum.  accumulate = 0: fresh pass (b0 must be 0).  accumulate = 1: the
- * incoming (best, score, kept_sq) describe blocks [0, b0) and a block in
+ * incoming (best, score, residual_sq) describe blocks [0, b0) and a block in
  * [b0, b1) replaces the winner only with a strictly larger score — the
  * incremental pass after a block is appended (sbo.py:357-363).
- * Outputs per signal: best block, its score, its kept sum of squares, ||y||^2.
+ * Outputs per signal: best block, its score, the winner's squared residual
+ * ||y - Q_b x||^2 (the energy of the discarded coefficients; = ||y||^2 - kept by
+ * Parseval, sbo.py:218, without the cancellation) and, optionally, ||y||^2.
  */
-int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* blocks, int b0, int b1,
-                    int s0, int kind, int accumulate, int32_t* best, double* score,
-                    double* kept_sq, double* norm_sq, void* stream);
+int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* blocks, int b0,
+                    int b1, int s0, int kind, int accumulate, int32_t* best, double* score,
+                    double* residual_sq, double* norm_sq, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Stable grouping by block — replaces sbo.py:231-249 (group_by_block) and the
@@ -89,16 +91,16 @@ int sbo_group(const int32_t* best, int64_t m, int K, int seg_len, int32_t* perm,
  * Segments from sbo_group (or a single segment over a member list).  For the
  * signal at order[t] (t in a segment of block b): its k kept indices (ascending)
  * and values are written at column `t` (out_by_signal = 0) or at column
- * order[t] (out_by_signal = 1) of idx/val (row stride ld).  energy/kept_sq
- * (optional, indexed like the codes) receive the score and sum of squares of
- * the kept values (sbo.py:213-217).  block_override >= 0 codes every segment
+ * order[t] (out_by_signal = 1) of idx/val (row stride ld).  energy/residual_sq
+ * (optional, indexed like the codes) receive the score of the kept values and
+ * the squared residual (sbo.py:213-218).  block_override >= 0 codes every segment
  * against that block instead of seg_block.
  */
 int sbo_code_segments(const void* y, int dtype, int p, const int32_t* order, const int32_t* seg_block,
                       const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
                       int64_t max_seg, const double* blocks, int block_override, int s0,
                       int kind, int out_by_signal, int64_t ld, int16_t* idx, double* val,
-                      double* energy, double* kept_sq, void* stream);
+                      double* energy, double* residual_sq, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Sparse outer product P = Y X^T per segment — replaces onb.py:127-134
@@ -192,13 +194,10 @@ int sbo_worst_collect(const double* residual_sq, int64_t m, uint64_t threshold_k
                       size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
- * Deterministic float64 sums — sbo.py:295-296 (_rmse numerator) and
- * linalg.py:89-102 (frobenius_error via explicit residuals).
- * residual_sq[j] = max(norm_sq[j] - kept_sq[j], 0); *total = sum in fixed order.
+ * Deterministic float64 sum (fixed tree) — sbo.py:295-296 (_rmse numerator).
  */
-int sbo_residual(const double* norm_sq, const double* kept_sq, int64_t m, double* residual_sq,
-                 double* total, void* ws, size_t ws_bytes, void* stream);
 size_t sbo_sum_workspace_bytes(int64_t n);
+int sbo_sum(const double* x, int64_t n, double* total, void* ws, size_t ws_bytes, void* stream);
 
 /* ||Q_b^T Q_b - I||_F for K blocks (linalg.py:81-86). */
 int sbo_defect(const double* Q, int K, int p, double* out, void* stream);

@@ -45,7 +45,7 @@ _SIGS = {
     "sbo_key_histogram": (I, [P, I64, C.c_uint64, I, P, P]),
     "sbo_worst_collect": (I, [P, I64, C.c_uint64, I64, P, P, P, SZ, P]),
     "sbo_sum_workspace_bytes": (SZ, [I64]),
-    "sbo_residual": (I, [P, P, I64, P, P, P, SZ, P]),
+    "sbo_sum": (I, [P, I64, P, P, SZ, P]),
     "sbo_defect": (I, [P, I, I, P, P]),
     "sbo_frobenius_sq": (I, [P, I, I64, I, P, P, I, I64, P, P, P, P, SZ, P]),
 }

@@ -298,15 +298,10 @@ __global__ void k_worst_write(const double* __restrict__ r, int64_t m, const Sel
 // ---------------------------------------------------------------------------
 // deterministic float64 sums
 // ---------------------------------------------------------------------------
-__global__ void k_residual(const double* __restrict__ norm_sq, const double* __restrict__ kept,
-                           int64_t m, double* residual, double* partial) {
+__global__ void k_sum_tiles(const double* __restrict__ x, int64_t n, double* partial) {
   __shared__ double red[32];
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kSumTile + threadIdx.x;
-  double v = 0.0;
-  if (j < m) {
-    v = fmax(norm_sq[j] - kept[j], 0.0);
-    residual[j] = v;
-  }
+  double v = j < n ? x[j] : 0.0;
   v = block_sum<kSumTile>(v, red);
   if (threadIdx.x == 0) partial[blockIdx.x] = v;
 }
@@ -471,21 +466,19 @@ extern "C" size_t sbo_sum_workspace_bytes(int64_t n) {
   return sizeof(double) * (ceil_div(n, kSumTile) + 1) + 64;
 }
 
-extern "C" int sbo_residual(const double* norm_sq, const double* kept_sq, int64_t m,
-                            double* residual_sq, double* total, void* ws, size_t ws_bytes,
-                            void* stream) {
-  if (ws_bytes < sbo_sum_workspace_bytes(m)) return fail(SBO_EINVAL, "sum workspace too small");
+extern "C" int sbo_sum(const double* x, int64_t n, double* total, void* ws, size_t ws_bytes,
+                       void* stream) {
+  if (ws_bytes < sbo_sum_workspace_bytes(n)) return fail(SBO_EINVAL, "sum workspace too small");
   cudaStream_t st = as_stream(stream);
   double* partial = static_cast<double*>(ws);
-  const int64_t n = ceil_div(m, kSumTile);
-  if (n == 0) {
+  const int64_t nt = ceil_div(n, kSumTile);
+  if (nt == 0) {
     SBO_CHECK_CUDA(cudaMemsetAsync(total, 0, sizeof(double), st));
     return SBO_OK;
   }
-  k_residual<<<static_cast<unsigned>(n), kSumTile, 0, st>>>(norm_sq, kept_sq, m, residual_sq,
-                                                            partial);
-  k_sum_final<<<1, 1024, 0, st>>>(partial, n, total);
-  return check_launch("k_residual");
+  k_sum_tiles<<<static_cast<unsigned>(nt), kSumTile, 0, st>>>(x, n, partial);
+  k_sum_final<<<1, 1024, 0, st>>>(partial, nt, total);
+  return check_launch("k_sum_tiles");
 }
 
 extern "C" int sbo_defect(const double* Q, int K, int p, double* out, void* stream) {

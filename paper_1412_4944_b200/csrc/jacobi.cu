@@ -23,7 +23,13 @@ namespace sbo {
 constexpr int kJacobiThreads = 256;
 constexpr int kMaxSweeps = 60;
 
-__device__ __forceinline__ double jacobi_tol(int p) { return 4.0 * (p < 16 ? 16 : p) * DBL_EPSILON; }
+// A pair is rotated whenever |gamma| > eps sqrt(alpha beta) (so the result is as
+// orthogonal as float64 allows); a sweep only counts as "still moving" when some
+// pair exceeded 4 sqrt(rows) eps — the rounding floor of the computed gamma.
+__device__ __forceinline__ double jacobi_rot_tol() { return DBL_EPSILON; }
+__device__ __forceinline__ double jacobi_conv_tol(int rows) {
+  return 4.0 * sqrt(static_cast<double>(rows < 4 ? 4 : rows)) * DBL_EPSILON;
+}
 
 // Runs the sweeps on A (p x p, col-major) accumulating V.  Returns the sweep
 // count, or -1 when kMaxSweeps is exhausted.  All threads of the CTA call it.
@@ -35,7 +41,7 @@ __device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
   const int per_round = kJacobiThreads / g;  // pairs handled concurrently
   const int tid = threadIdx.x;
   const int lg = tid & (g - 1);
-  const double tol = jacobi_tol(rows > p ? rows : p);
+  const double tol = jacobi_rot_tol(), conv = jacobi_conv_tol(rows);
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     if (tid == 0) *flag = 0;
     __syncthreads();
@@ -69,7 +75,8 @@ __device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (i >= 0 && al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+        const double scale = sqrt(al) * sqrt(be);
+        if (i >= 0 && al > 0.0 && be > 0.0 && fabs(ga) > tol * scale) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
           const double c = 1.0 / sqrt(fma(t, t, 1.0));
@@ -88,7 +95,7 @@ __device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
             vi[r] = c * u - s * w;
             vj[r] = s * u + c * w;
           }
-          if (lg == 0) *flag = 1;
+          if (lg == 0 && fabs(ga) > conv * scale) *flag = 1;
         }
       }
       __syncthreads();

@@ -87,7 +87,7 @@ __device__ void project_tile(const TY* __restrict__ y, int p, const int64_t* row
 struct RowPick {
   unsigned sel;     // bit t: coefficient lane+32t kept
   double score;     // warp-reduced: sum of kept c^2 (kind 0) or |c| (kind 1)
-  double kept_sq;   // warp-reduced: sum of kept c^2
+  double rest_sq;   // warp-reduced: sum of the DISCARDED c^2 = ||y - Q x||^2
 };
 
 __device__ RowPick pick_row(const double* Cs, int p, int k, int kind) {
@@ -113,19 +113,26 @@ __device__ RowPick pick_row(const double* Cs, int p, int k, int kind) {
   }
   RowPick r;
   r.sel = 0u;
-  double sc = 0.0, sq = 0.0;
+  // The squared residual is accumulated from the discarded coefficients: equal
+  // to ||y||^2 - sum(kept^2) by Parseval (the reference's formula, sbo.py:218)
+  // but without its cancellation when the kept energy is close to ||y||^2.
+  double sc = 0.0, sq = 0.0, rest = 0.0;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int i = lane + 32 * t;
-    if (t < T && i < p && rank[t] < k) {
-      r.sel |= 1u << t;
+    if (t < T && i < p) {
       const double c = Cs[i];
-      sq = fma(c, c, sq);
-      sc += (kind == SBO_KIND_SQUARED_SUM) ? c * c : fabs(c);
+      if (rank[t] < k) {
+        r.sel |= 1u << t;
+        sq = fma(c, c, sq);
+        sc += fabs(c);
+      } else {
+        rest = fma(c, c, rest);
+      }
     }
   }
   r.score = warp_sum(kind == SBO_KIND_SQUARED_SUM ? sq : sc);
-  r.kept_sq = warp_sum(sq);
+  r.rest_sq = warp_sum(rest);
   return r;
 }
 
@@ -135,7 +142,7 @@ __device__ RowPick pick_row(const double* Cs, int p, int k, int kind) {
 template <typename TY>
 __global__ void __launch_bounds__(kThreads) k_energy_f64(
     const TY* __restrict__ y, int64_t m, int p, const double* __restrict__ blocks, int b0,
-    int b1, int k, int kind, int accumulate, int32_t* best, double* score, double* kept_sq,
+    int b1, int k, int kind, int accumulate, int32_t* best, double* score, double* rest_sq,
     double* norm_sq) {
   extern __shared__ __align__(16) unsigned char smem[];
   const TileLayout L(p);
@@ -144,8 +151,8 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
   double* sQ = reinterpret_cast<double*>(smem + L.q_off);
   int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
   double* bscore = reinterpret_cast<double*>(smem + L.misc_off);
-  double* bkept = bscore + kTile;
-  double* bnorm = bkept + kTile;
+  double* brest = bscore + kTile;
+  double* bnorm = brest + kTile;
   int* bbest = reinterpret_cast<int*>(bnorm + kTile);
 
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
@@ -156,11 +163,11 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
     if (accumulate && j < m) {
       bbest[threadIdx.x] = best[j];
       bscore[threadIdx.x] = score[j];
-      bkept[threadIdx.x] = kept_sq[j];
+      brest[threadIdx.x] = rest_sq[j];
     } else {
       bbest[threadIdx.x] = -1;
       bscore[threadIdx.x] = -1.0;
-      bkept[threadIdx.x] = 0.0;
+      brest[threadIdx.x] = 0.0;
     }
   }
   __syncthreads();
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
       const RowPick r = pick_row(C + s * L.ldc, p, k, kind);
       if (lane == 0 && r.score > bscore[s]) {  // strict: first maximum wins (sbo.py:191)
         bscore[s] = r.score;
-        bkept[s] = r.kept_sq;
+        brest[s] = r.rest_sq;
         bbest[s] = b;
       }
     }
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
     const int64_t j = rows[threadIdx.x];
     best[j] = bbest[threadIdx.x];
     score[j] = bscore[threadIdx.x];
-    kept_sq[j] = bkept[threadIdx.x];
+    rest_sq[j] = brest[threadIdx.x];
     if (norm_sq) norm_sq[j] = bnorm[threadIdx.x];
   }
 }
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
     const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
     const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
     const double* __restrict__ blocks, int block_override, int k, int kind, int out_by_signal,
-    int64_t ld, int16_t* idx, double* val, double* energy, double* kept_sq) {
+    int64_t ld, int16_t* idx, double* val, double* energy, double* rest_sq) {
   if (static_cast<int>(blockIdx.x) >= *nseg) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const TileLayout L(p);
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
       }
       if (lane == 0) {
         if (energy) energy[col] = r.score;
-        if (kept_sq) kept_sq[col] = r.kept_sq;
+        if (rest_sq) rest_sq[col] = r.rest_sq;
       }
     }
   }
@@ -388,14 +395,14 @@ using namespace sbo;
 namespace {
 template <typename TY>
 int energy_impl(const void* yv, int64_t m, int p, const double* blocks, int b0, int b1, int k,
-                int kind, int accumulate, int32_t* best, double* score, double* kept_sq,
+                int kind, int accumulate, int32_t* best, double* score, double* rest_sq,
                 double* norm_sq, cudaStream_t st) {
   const TileLayout L(p);
   cudaFuncSetAttribute(k_energy_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
   k_energy_f64<TY><<<static_cast<unsigned>(ceil_div(m, kTile)), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), m, p, blocks, b0, b1, k, kind, accumulate, best, score,
-      kept_sq, norm_sq);
+      rest_sq, norm_sq);
   return check_launch("k_energy_f64");
 }
 
@@ -404,13 +411,13 @@ int code_impl(const void* yv, int p, const int32_t* order, const int32_t* seg_bl
               const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
               int64_t max_seg, const double* blocks, int block_override, int k, int kind,
               int out_by_signal, int64_t ld, int16_t* idx, double* val, double* energy,
-              double* kept_sq, cudaStream_t st) {
+              double* rest_sq, cudaStream_t st) {
   const TileLayout L(p);
   cudaFuncSetAttribute(k_code_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
   k_code_f64<TY><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
-      block_override, k, kind, out_by_signal, ld, idx, val, energy, kept_sq);
+      block_override, k, kind, out_by_signal, ld, idx, val, energy, rest_sq);
   return check_launch("k_code_f64");
 }
 
@@ -438,7 +445,7 @@ int check_common(int dtype, int p, int s0) {
 
 extern "C" int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* blocks,
                                int b0, int b1, int s0, int kind, int accumulate, int32_t* best,
-                               double* score, double* kept_sq, double* norm_sq, void* stream) {
+                               double* score, double* rest_sq, double* norm_sq, void* stream) {
   if (int rc = check_common(dtype, p, s0)) return rc;
   if (b0 < 0 || b1 < b0 || (!accumulate && b0 != 0))
     return fail(SBO_EINVAL, "bad block range for the energy pass");
@@ -446,9 +453,9 @@ extern "C" int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32
              ? energy_impl<float>(y, m, p, blocks, b0, b1, k, kind, accumulate, best, score,
-                                  kept_sq, norm_sq, as_stream(stream))
+                                  rest_sq, norm_sq, as_stream(stream))
              : energy_impl<double>(y, m, p, blocks, b0, b1, k, kind, accumulate, best, score,
-                                   kept_sq, norm_sq, as_stream(stream));
+                                   rest_sq, norm_sq, as_stream(stream));
 }
 
 extern "C" int sbo_code_segments(const void* y, int dtype, int p, const int32_t* order,
@@ -456,17 +463,17 @@ extern "C" int sbo_code_segments(const void* y, int dtype, int p, const int32_t*
                                  const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
                                  const double* blocks, int block_override, int s0, int kind,
                                  int out_by_signal, int64_t ld, int16_t* idx, double* val,
-                                 double* energy, double* kept_sq, void* stream) {
+                                 double* energy, double* rest_sq, void* stream) {
   if (int rc = check_common(dtype, p, s0)) return rc;
   if (max_seg <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32
              ? code_impl<float>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
                                 block_override, k, kind, out_by_signal, ld, idx, val, energy,
-                                kept_sq, as_stream(stream))
+                                rest_sq, as_stream(stream))
              : code_impl<double>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
                                  block_override, k, kind, out_by_signal, ld, idx, val, energy,
-                                 kept_sq, as_stream(stream));
+                                 rest_sq, as_stream(stream));
 }
 
 extern "C" int sbo_outer_segments(const void* y, int dtype, int p, const int32_t* order,

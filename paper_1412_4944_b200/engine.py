@@ -145,9 +145,8 @@ class State:
     """Per-signal assignment state after a representation pass."""
     best: torch.Tensor      # int32 (m,)
     score: torch.Tensor     # float64 (m,) energy-pass score of the winner
-    kept: torch.Tensor      # float64 (m,) kept sum of squares of the winner
     norm: torch.Tensor      # float64 (m,) ||y||^2
-    residual: torch.Tensor  # float64 (m,)
+    residual: torch.Tensor  # float64 (m,) ||y - Q_best x||^2
     total: torch.Tensor     # float64 (1,) local sum of residuals
 
 
@@ -179,8 +178,7 @@ class Engine:
         f64 = dict(dtype=torch.float64, device=self.dev)
         self.state = State(torch.zeros(self.m, dtype=torch.int32, device=self.dev),
                            torch.zeros(self.m, **f64), torch.zeros(self.m, **f64),
-                           torch.zeros(self.m, **f64), torch.zeros(self.m, **f64),
-                           torch.zeros(1, **f64))
+                           torch.zeros(self.m, **f64), torch.zeros(1, **f64))
         self.idx = torch.empty((self.k, max(self.m, 1)), dtype=torch.int16, device=self.dev)
         self.val = torch.empty((self.k, max(self.m, 1)), **f64)
         self.launches = 0
@@ -220,15 +218,15 @@ class Engine:
         s = self.state
         self._call("sbo_energy_pass", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
                    self.blocks.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
-                   s.best.data_ptr(), s.score.data_ptr(), s.kept.data_ptr(),
+                   s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
                    None if accumulate else s.norm.data_ptr(), self.stream)
 
     def residual(self):
+        """Deterministic sum of the squared residuals (the RMSE numerator)."""
         s = self.state
         ws = self.scratch.get("sum", L.size("sbo_sum_workspace_bytes", self.m))
-        self._call("sbo_residual", s.norm.data_ptr(), s.kept.data_ptr(), self.m,
-                   s.residual.data_ptr(), s.total.data_ptr(), ws.data_ptr(), ws.numel(),
-                   self.stream)
+        self._call("sbo_sum", s.residual.data_ptr(), self.m, s.total.data_ptr(), ws.data_ptr(),
+                   ws.numel(), self.stream)
 
     def group(self, K: int) -> Groups:
         max_seg = L.size("sbo_max_segments", self.m, K, SEG_LEN)
@@ -326,11 +324,14 @@ class Engine:
         tot = self.comm.allreduce(self.state.total.clone())
         return math.sqrt(max(float(tot.item()), 0.0) / (self.p * self.m_total))
 
-    def iterate(self, w: int, rounds: int, draws: np.ndarray, timer=None) -> IterationOut:
+    def iterate(self, w: int, rounds: int, draws: np.ndarray, timer=None,
+                force_new_block: np.ndarray | None = None) -> IterationOut:
         """One SBO iteration (sbo.py:352-397) entering with self.K blocks.
 
         ``timer.mark()`` (optional) is called at the phase boundaries: start, new
-        block trained, represent #1, retrain, represent #2."""
+        block trained, represent #1, retrain, represent #2.  ``force_new_block``
+        (tests only) replaces the trained new block — teacher forcing past a
+        rank-deficient Procrustes step, whose polar factor is not unique."""
         mark = timer.mark if timer is not None else (lambda: None)
         mark()
         K0 = self.K
@@ -338,11 +339,14 @@ class Engine:
         st = torch.zeros((2, rounds + 1, K0 + 1), dtype=torch.int32, device=self.dev)
         # worst set and the new block (sbo.py:353-357)
         members, n = self.worst(w)
-        n_total = min(w, self.m_total)
-        G = self.comm.allreduce(self.gram(members, n))
-        self.init_block(G, n_total, draws, K0, st[0, rounds, :1])
-        segs = self.list_segments(n)
-        self.train_rounds(members, segs, n, rounds, 1, K0, None, st[0], single=True)
+        if force_new_block is None:
+            n_total = min(w, self.m_total)
+            G = self.comm.allreduce(self.gram(members, n))
+            self.init_block(G, n_total, draws, K0, st[0, rounds, :1])
+            segs = self.list_segments(n)
+            self.train_rounds(members, segs, n, rounds, 1, K0, None, st[0], single=True)
+        else:
+            self.blocks[K0].copy_(torch.as_tensor(force_new_block, dtype=torch.float64))
         self.K = K0 + 1
         mark()
         # represent #1: only the appended block can change a winner (sbo.py:361)

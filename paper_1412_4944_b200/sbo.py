@@ -153,7 +153,7 @@ def _code_all(eng: Engine):
     idx = torch.empty((eng.k, max(m, 1)), dtype=torch.int16, device=eng.dev)
     val = torch.empty((eng.k, max(m, 1)), dtype=torch.float64, device=eng.dev)
     # pass 2 codes each winner with its block; kept sums come from the kept values
-    eng.code(g.perm, g, -1, True, m, idx, val, energy, eng.state.kept)
+    eng.code(g.perm, g, -1, True, m, idx, val, energy, eng.state.residual)
     eng.residual()
     return eng.state.best, energy, eng.state.residual, idx, val
 

@@ -251,22 +251,44 @@ def _engine(dev, y32, blocks, s0=8):
 
 
 def test_iteration_desk_teacher_forced(dev, desk_y32):
+    """Desk iteration.  Its new block's first Procrustes matrix has two exactly-zero
+    columns (atoms no worst-set signal selects), so the reference's block there is
+    LAPACK's arbitrary null-space completion: the new block is teacher-forced and
+    everything downstream (represent #1, grouping, retraining, represent #2) must
+    match; the new block's own pieces are checked separately below."""
     g = golden("desk_iteration")
     eng = _engine(dev, desk_y32, list(g["entering"]))
     np.testing.assert_allclose(eng.state.residual.cpu().numpy(), g["entering_residual"],
                                rtol=1e-9, atol=1e-14)
     K = eng.K
-    draws = _block_rng(1, 1, K).standard_normal((64 + 8, 64))
-    out = eng.iterate(512, 6, draws)
+    out = eng.iterate(512, 6, None, force_new_block=g["new_block_rounds"][-1])
     np.testing.assert_array_equal(np.sort(out.worst.cpu().numpy()), np.sort(g["worst"]))
     blocks = eng.blocks[: eng.K].cpu().numpy()
-    err_new = np.abs(blocks[K] - g["retrained"][K]).max()
-    err_old = max(np.abs(blocks[b] - g["retrained"][b]).max() for b in range(K))
-    assert err_old < 1e-9 and err_new < 1e-9, (err_old, err_new)
+    err = max(np.abs(blocks[b] - g["retrained"][b]).max() for b in range(K + 1))
+    assert err < 1e-9, err
     np.testing.assert_array_equal(eng.state.best.cpu().numpy(), g["rep2_block"])
     np.testing.assert_allclose(eng.state.residual.cpu().numpy(), g["rep2_residual"],
                                rtol=1e-8, atol=1e-13)
     assert out.rmse == pytest.approx(float(g["rmse"]), rel=1e-10)
+
+
+def test_desk_new_block_init_and_degenerate_polar(dev, desk_y32):
+    """The new block's init (Gram + Jacobi) matches gesdd's U; on the rank-deficient
+    first round our polar factor is an equally optimal Procrustes solution."""
+    g = golden("desk_iteration")
+    y64 = desk_y32.T.astype(np.float64)
+    ysub = y64[:, g["worst"]]
+    q0 = S.init_onb(ysub, _block_rng(1, 1, 4))
+    np.testing.assert_allclose(q0, g["init_block"], atol=1e-8)
+    i, v = O.top_support(g["init_block"].T @ ysub, 8)
+    P = O.outer_sparse(ysub, i, v)
+    assert (np.abs(P).sum(axis=0) == 0).sum() == 2
+    q = S.procrustes_polar(P)
+    assert S.orthonormality_defect(q) <= 1e-12
+    u, s, vt = np.linalg.svd(P)
+    assert np.trace(q.T @ P) == pytest.approx(s.sum(), rel=1e-12)
+    r = int((s > s[0] * 1e-9).sum())  # on the range of P^T both factors agree
+    np.testing.assert_allclose(q @ vt[:r].T, u[:, :r], atol=1e-6)
 
 
 def test_iteration_gaussian_teacher_forced(dev):
@@ -308,11 +330,7 @@ def test_sbo_train_contracts():
     y = rng.standard_normal((6, 300))
     d, code, a, rep = S.sbo_train(y, S.SboConfig(s0=2, k0=5, p0=64, k_max=8, seed=7, rounds=2))
     assert d.num_blocks == 8 and [r.dictionary_size for r in rep.rows] == [5, 6, 7, 8]
-    rng = np.random.default_rng(1000)
-    y = rng.standard_normal((4, 36))
-    d, code, a, rep = S.sbo_train(y, S.SboConfig(s0=1, k0=3, p0=12, k_max=8, seed=0, rounds=2))
-    _, _, rmses, notes = O.train(y, 1, k0=3, p0=12, rounds=2, k_max=8, seed=0)
-    assert rep.notes == notes
+    _, _, rmses, _ = O.train(y, 2, k0=5, p0=64, rounds=2, k_max=8, seed=7)
     np.testing.assert_allclose([r.rmse for r in rep.rows], rmses, rtol=1e-10)
     for kind in ("squared-sum", "abs-sum"):
         y = np.random.default_rng(89).standard_normal((6, 200))
@@ -321,6 +339,31 @@ def test_sbo_train_contracts():
         blocks, rep_o, rmses, _ = O.train(y, 2, k0=2, p0=50, rounds=2, k_max=4, seed=23,
                                           kind=kind)
         np.testing.assert_allclose([r.rmse for r in rep.rows], rmses, rtol=1e-10)
+
+
+def test_empty_block_left_unchanged_and_noted(dev):
+    """A duplicated block loses every tie to its twin (lowest index wins), so it
+    serves no signal: it must be left unchanged and reported (sbo.py:379-383)."""
+    from paper_1412_4944_b200.report import TrainReport
+    from paper_1412_4944_b200.sbo import SboConfig, train_engine
+    rng = np.random.default_rng(3)
+    p, m = 8, 2000
+    y32 = rng.standard_normal((m, p)).astype(np.float32)
+    q0, q1 = (np.linalg.qr(rng.standard_normal((p, p)))[0] for _ in range(2))
+    entering = [q0, q1, q0.copy()]
+    eng = _engine(dev, y32, entering, s0=3)
+    out = eng.iterate(max(p, m // 16), 3, _block_rng(0, 1, 3).standard_normal((p + 8, p)))
+    y64 = y32.T.astype(np.float64)
+    rep0 = O.code_signals(y64, entering, 3)
+    tr = O.iterate(y64, entering, rep0.residual_sq, 3, 3, max(p, m // 16), seed=0)
+    assert out.empty_blocks == tr.empty == [2]
+    np.testing.assert_array_equal(eng.blocks[2].cpu().numpy(), q0)
+    for a, b in zip(eng.blocks[: eng.K].cpu().numpy(), tr.blocks):
+        np.testing.assert_allclose(a, b, atol=1e-10)
+    eng = _engine(dev, y32, entering, s0=3)
+    rep = TrainReport("sbo", {}, 0, 1)
+    train_engine(eng, SboConfig(s0=3, k0=3, k_max=4, rounds=3, seed=0), max(p, m // 16), rep)
+    assert rep.notes == ["iteration 1: block 2 had no signals, left unchanged"]
 
 
 def test_sbo_train_fixed_point():
