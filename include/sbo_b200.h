@@ -71,6 +71,35 @@ int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* bl
                     int b1, int s0, int kind, int accumulate, int32_t* best, double* score,
                     double* residual_sq, double* norm_sq, void* stream);
 
+/* Exact float64 re-decision of the signals list[0 .. *nlist) over all K blocks:
+ * rewrites their best / score / residual_sq (the certification step after the
+ * tensor-core energy pass flags near-ties).  max_list bounds *nlist (grid size). */
+int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p, const double* blocks, int K,
+                       int s0, int kind, const int32_t* list, const int32_t* nlist,
+                       int64_t max_list, int32_t* best, double* score, double* residual_sq,
+                       void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Tensor-core energy pass, p = 64 (tc_energy.cu) — the same contract as
+ * sbo_energy_pass on split-fp16 operands with fp32 accumulation in TMEM:
+ *   sbo_tc_split_signals: y -> yh, yl (fp16 hi/lo, 128-B rows pre-swizzled) and a
+ *     per-signal power-of-two scale; arrays sized sbo_tc_padded_rows(m) rows.
+ *   sbo_tc_split_blocks:  K blocks -> qh, ql (atom rows, pre-swizzled) + scales.
+ *   sbo_tc_energy: best block per signal with an error-bounded certificate;
+ *     signals whose decision is within the bound are appended to flags
+ *     (count in *nflag, which the caller zeroes) for sbo_energy_recheck.
+ *     score / residual_sq of unflagged signals are float32-accurate.
+ */
+int64_t sbo_tc_padded_rows(int64_t m);
+int sbo_tc_split_signals(const void* y, int dtype, int64_t m, int p, void* yh, void* yl,
+                         int16_t* escale, void* stream);
+int sbo_tc_split_blocks(const double* Q, int K, int p, void* qh, void* ql, int16_t* fscale,
+                        void* stream);
+int sbo_tc_energy(const void* yh, const void* yl, const int16_t* escale, int64_t m,
+                  const void* qh, const void* ql, const int16_t* fscale, int b0, int b1, int s0,
+                  int kind, int accumulate, int32_t* best, double* score, double* residual_sq,
+                  int32_t* flags, int32_t* nflag, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Stable grouping by block — replaces sbo.py:231-249 (group_by_block) and the
  * argsort/searchsorted of sbo.py:200-201.  perm lists signals block by block,
@@ -138,13 +167,16 @@ int sbo_select_top(const double* coeffs, int64_t t, int p, int s0, int64_t ld, i
  * linalg.py:68-78 (procrustes_polar via thin_svd/gesdd) and the guard of
  * onb.py:119-124.  One-sided Jacobi (Hestenes) in float64.  Q (K x p x p) is
  * updated in place; blocks with counts[b] == 0 (counts may be NULL) are left
- * unchanged and flagged SBO_ST_SKIPPED (sbo.py:379-383).  sigma (optional,
- * K x p) receives the singular values in descending order.
+ * unchanged and flagged SBO_ST_SKIPPED (sbo.py:379-383).  V (optional, K x p x p
+ * column-major, in/out) warm-starts the rotation from the previous round's
+ * right singular vectors and receives the new ones (the identity is a valid
+ * first guess).  sigma (optional, K x p) receives the singular values in
+ * descending order.  status[b]: low byte SBO_ST_*, bits 8..15 sweeps used.
  * Workspace: sbo_polar_workspace_bytes(K, p).
  */
 size_t sbo_polar_workspace_bytes(int K, int p);
-int sbo_polar(const double* P, int K, int p, const int64_t* counts, double* Q, double* sigma,
-              int32_t* status, void* ws, size_t ws_bytes, void* stream);
+int sbo_polar(const double* P, int K, int p, const int64_t* counts, double* Q, double* V,
+              double* sigma, int32_t* status, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * New block initialisation from a Gram matrix — replaces onb.py:79-116

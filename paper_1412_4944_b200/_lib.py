@@ -25,6 +25,11 @@ _SIGS = {
     "sbo_last_error": (C.c_char_p, []),
     "sbo_device_ok": (I, [I]),
     "sbo_energy_pass": (I, [P, I, I64, I, P, I, I, I, I, I, P, P, P, P, P]),
+    "sbo_energy_recheck": (I, [P, I, I64, I, P, I, I, I, P, P, I64, P, P, P, P]),
+    "sbo_tc_padded_rows": (I64, [I64]),
+    "sbo_tc_split_signals": (I, [P, I, I64, I, P, P, P, P]),
+    "sbo_tc_split_blocks": (I, [P, I, I, P, P, P, P]),
+    "sbo_tc_energy": (I, [P, P, P, I64, P, P, P, I, I, I, I, I, P, P, P, P, P, P]),
     "sbo_group_workspace_bytes": (SZ, [I64, I]),
     "sbo_max_segments": (I64, [I64, I, I]),
     "sbo_group": (I, [P, I64, I, I, P, P, P, P, P, P, P, SZ, P]),
@@ -35,7 +40,7 @@ _SIGS = {
     "sbo_gram": (I, [P, I, I, P, I64, I, P, P, SZ, P]),
     "sbo_select_top": (I, [P, I64, I, I, I64, P, P, P]),
     "sbo_polar_workspace_bytes": (SZ, [I, I]),
-    "sbo_polar": (I, [P, I, I, P, P, P, P, P, SZ, P]),
+    "sbo_polar": (I, [P, I, I, P, P, P, P, P, P, SZ, P]),
     "sbo_init_workspace_bytes": (SZ, [I]),
     "sbo_init_block": (I, [P, I, I64, P, I, P, P, P, P, SZ, P]),
     "sbo_svd_workspace_bytes": (SZ, [I, I]),

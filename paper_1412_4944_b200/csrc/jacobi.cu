@@ -31,9 +31,83 @@ __device__ __forceinline__ double jacobi_conv_tol(int rows) {
   return 4.0 * sqrt(static_cast<double>(rows < 4 ? 4 : rows)) * DBL_EPSILON;
 }
 
+// Rotation of one column pair: t = tan(theta) in fp32 from power-of-two-scaled
+// inputs (no overflow, no float64 division chain), then c, s normalized in
+// float64 so c^2 + s^2 = 1 to rounding and V stays orthogonal; an fp32-accurate
+// angle only leaves ~1e-7 gamma for the next sweep.
+__device__ __forceinline__ void rotation(double al, double be, double ga, double& c, double& s) {
+  const double d = be - al, gg = 2.0 * ga;
+  int ex;
+  frexp(fmax(fabs(d), fabs(gg)), &ex);
+  const float df = static_cast<float>(ldexp(d, -ex));
+  const float gf = static_cast<float>(ldexp(gg, -ex));
+  const float tf = copysignf(1.0f, df) * gf / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+  const double t = static_cast<double>(tf);
+  c = rsqrt(fma(t, t, 1.0));
+  s = c * t;
+}
+
+// p = 64 specialization: 32 column pairs per step, 8 lanes per pair, lane lg
+// owns rows lg + 8u; the round-robin schedule advances incrementally and the
+// pair's rows stay in registers between the dot products and the rotation.
+__device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) {
+  constexpr int N = 64;
+  const int tid = threadIdx.x, q = tid >> 3, lg = tid & 7;
+  const double tol2 = DBL_EPSILON * DBL_EPSILON;
+  const double conv = 4.0 * 8.0 * DBL_EPSILON, conv2 = conv * conv;
+  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    int i = q, j = q == 0 ? N - 1 : N - 1 - q;  // step 0 of the tournament
+    for (int step = 0; step < N - 1; ++step) {
+      double* ai = A + i * N + lg;
+      double* aj = A + j * N + lg;
+      double x[8], y[8], al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        x[u] = ai[8 * u];
+        y[u] = aj[8 * u];
+        al = fma(x[u], x[u], al);
+        be = fma(y[u], y[u], be);
+        ga = fma(x[u], y[u], ga);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      const double g2 = ga * ga, ab = al * be;
+      if (al > 0.0 && be > 0.0 && g2 > tol2 * ab) {
+        double c, s;
+        rotation(al, be, ga, c, s);
+        double* vi = V + i * N + lg;
+        double* vj = V + j * N + lg;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          ai[8 * u] = c * x[u] - s * y[u];
+          aj[8 * u] = s * x[u] + c * y[u];
+          const double vu = vi[8 * u], vw = vj[8 * u];
+          vi[8 * u] = c * vu - s * vw;
+          vj[8 * u] = s * vu + c * vw;
+        }
+        if (lg == 0 && g2 > conv2 * ab) *flag = 1;
+      }
+      __syncthreads();
+      // next step: i, j advance by one modulo 63 (slot 0 keeps j = 63)
+      i = (i == N - 2) ? 0 : i + 1;
+      if (q != 0) j = (j == N - 2) ? 0 : j + 1;
+    }
+    if (*flag == 0) return sweep + 1;
+    __syncthreads();
+  }
+  return -1;
+}
+
 // Runs the sweeps on A (p x p, col-major) accumulating V.  Returns the sweep
 // count, or -1 when kMaxSweeps is exhausted.  All threads of the CTA call it.
-__device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
+__device__ __forceinline__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
+  if (rows == 64 && p == 64 && blockDim.x == 256) return jacobi_sweeps64(A, V, flag);
   const int n = p + (p & 1);
   const int npairs = n >> 1;
   int g = 32;
@@ -75,11 +149,20 @@ __device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        const double scale = sqrt(al) * sqrt(be);
-        if (i >= 0 && al > 0.0 && be > 0.0 && fabs(ga) > tol * scale) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double c = 1.0 / sqrt(fma(t, t, 1.0));
+        const double g2 = ga * ga, ab = al * be;
+        if (i >= 0 && al > 0.0 && be > 0.0 && g2 > tol * tol * ab) {
+          // Rotation angle t = tan(theta) in fp32 from power-of-two-scaled inputs
+          // (no overflow, no float64 division chain); c, s are then normalized in
+          // float64 so c^2 + s^2 = 1 to rounding and V stays orthogonal.  An
+          // fp32-accurate angle only leaves ~1e-7 gamma for the next sweep.
+          const double d = be - al, gg = 2.0 * ga;
+          int ex;
+          frexp(fmax(fabs(d), fabs(gg)), &ex);
+          const float df = static_cast<float>(ldexp(d, -ex));
+          const float gf = static_cast<float>(ldexp(gg, -ex));
+          const float tf = copysignf(1.0f, df) * gf / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+          const double t = static_cast<double>(tf);
+          const double c = rsqrt(fma(t, t, 1.0));
           const double s = c * t;
           double* ai = A + static_cast<int64_t>(i) * rows;
           double* aj = A + static_cast<int64_t>(j) * rows;
@@ -95,7 +178,7 @@ __device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
             vi[r] = c * u - s * w;
             vj[r] = s * u + c * w;
           }
-          if (lg == 0 && fabs(ga) > conv * scale) *flag = 1;
+          if (lg == 0 && g2 > conv * conv * ab) *flag = 1;
         }
       }
       __syncthreads();
@@ -107,7 +190,7 @@ __device__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
 }
 
 // norms of the columns of A -> sig[j]; descending order with index tie-break -> ord
-__device__ void column_order(const double* A, int rows, int p, double* sig, int* ord,
+__device__ __forceinline__ void column_order(const double* A, int rows, int p, double* sig, int* ord,
                              bool sqrt_norm) {
   for (int j = threadIdx.x; j < p; j += blockDim.x) {
     const double* a = A + static_cast<int64_t>(j) * rows;
@@ -125,7 +208,7 @@ __device__ void column_order(const double* A, int rows, int p, double* sig, int*
 }
 
 // orthonormality defect of a row-major p x p matrix (CTA-wide, deterministic)
-__device__ double defect_of(const double* Q, int p, double* red) {
+__device__ __forceinline__ double defect_of(const double* Q, int p, double* red) {
   double acc = 0.0;
   for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
     const int a = e / p, b = e % p;
@@ -144,11 +227,12 @@ struct JacobiSmem {
   int count;
 };
 
+template <bool SMEM>
 __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restrict__ P, int p,
                                                           const int64_t* __restrict__ counts,
-                                                          double* Q, double* sigma_out,
-                                                          int32_t* status, double* ws,
-                                                          int use_smem) {
+                                                          double* Q, double* Vio,
+                                                          double* sigma_out, int32_t* status,
+                                                          double* ws, int use_smem) {
   const int b = blockIdx.x;
   const int64_t pp = static_cast<int64_t>(p) * p;
   __shared__ JacobiSmem S;
@@ -161,7 +245,7 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
   double* V;
   double* sig;
   int* ord;
-  if (use_smem) {
+  if constexpr (SMEM) {  // compile-time: shared accesses compile to LDS/STS
     A = reinterpret_cast<double*>(dyn);
     V = A + pp;
     sig = V + pp;
@@ -173,14 +257,32 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
     ord = reinterpret_cast<int*>(sig + p);
   }
   const double* Pb = P + b * pp;
-  // A = P in column-major (a_j = column j of P); V = I
-  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
-    const int r = static_cast<int>(e / p), c = static_cast<int>(e % p);
-    A[static_cast<int64_t>(c) * p + r] = Pb[e];
-    V[static_cast<int64_t>(c) * p + r] = (r == c) ? 1.0 : 0.0;
+  double* Vb = Vio ? Vio + b * pp : nullptr;
+  if (Vb) {
+    // warm start: A = P V_prev (columns nearly orthogonal when P moved little
+    // since the previous round), V = V_prev; V_prev is column-major
+    for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) V[e] = Vb[e];
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+      const int j = static_cast<int>(e / p), r = static_cast<int>(e % p);
+      const double* pr = Pb + static_cast<int64_t>(r) * p;
+      const double* vj = V + static_cast<int64_t>(j) * p;
+      double acc = 0.0;
+      for (int c = 0; c < p; ++c) acc = fma(pr[c], vj[c], acc);
+      A[e] = acc;
+    }
+  } else {
+    // cold start: A = P in column-major (a_j = column j of P); V = I
+    for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+      const int r = static_cast<int>(e / p), c = static_cast<int>(e % p);
+      A[static_cast<int64_t>(c) * p + r] = Pb[e];
+      V[static_cast<int64_t>(c) * p + r] = (r == c) ? 1.0 : 0.0;
+    }
   }
   __syncthreads();
   const int sweeps = jacobi_sweeps(A, V, p, p, &S.flag);
+  if (Vb)
+    for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) Vb[e] = V[e];
   column_order(A, p, p, sig, ord, true);
   const double smax = sig[ord[0]];
   const double null_tol = smax * 64.0 * DBL_EPSILON;
@@ -233,12 +335,14 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
     for (int r = threadIdx.x; r < p; r += blockDim.x) sigma_out[b * p + r] = sig[ord[r]];
   __syncthreads();
   const double d = defect_of(Qb, p, S.red);
-  if (threadIdx.x == 0 && status) {
-    status[b] = sweeps < 0 ? SBO_ST_NOCONV : (!(d <= 1e-8) ? SBO_ST_DEFECT : SBO_ST_OK);
+  if (threadIdx.x == 0 && status) {  // low byte: status, bits 8..15: sweeps used
+    const int code = sweeps < 0 ? SBO_ST_NOCONV : (!(d <= 1e-8) ? SBO_ST_DEFECT : SBO_ST_OK);
+    status[b] = code | ((sweeps < 0 ? kMaxSweeps : sweeps) << 8);
   }
 }
 
 // ---------------------------------------------------------------------------
+template <bool SMEM>
 __global__ void __launch_bounds__(kJacobiThreads) k_init_block(
     const double* __restrict__ G, int p, int64_t ncols, const double* __restrict__ draws,
     int ndraws, double* Q, int32_t* rank_out, int32_t* status, double* ws, int use_smem) {
@@ -247,7 +351,9 @@ __global__ void __launch_bounds__(kJacobiThreads) k_init_block(
   extern __shared__ __align__(16) unsigned char dyn[];
   double *A, *V, *lam, *U;
   int* ord;
-  double* base = use_smem ? reinterpret_cast<double*>(dyn) : ws;
+  double* base;
+  if constexpr (SMEM) base = reinterpret_cast<double*>(dyn);
+  else base = ws;
   A = base;
   V = A + pp;
   U = V + pp;
@@ -335,7 +441,8 @@ __global__ void __launch_bounds__(kJacobiThreads) k_init_block(
       rank_out[1] = d;  // completion draws consumed
     }
     if (status)
-      *status = (sweeps < 0 || ran_out) ? SBO_ST_NOCONV : (!(df <= 1e-8) ? SBO_ST_DEFECT : SBO_ST_OK);
+      *status = ((sweeps < 0 || ran_out) ? SBO_ST_NOCONV : (!(df <= 1e-8) ? SBO_ST_DEFECT : SBO_ST_OK)) |
+                ((sweeps < 0 ? kMaxSweeps : sweeps) << 8);
   }
 }
 
@@ -360,16 +467,22 @@ extern "C" size_t sbo_polar_workspace_bytes(int K, int p) {
 }
 
 extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, double* Q,
-                         double* sigma, int32_t* status, void* ws, size_t ws_bytes,
+                         double* V, double* sigma, int32_t* status, void* ws, size_t ws_bytes,
                          void* stream) {
   if (K < 1 || p < 1 || p > kPMax) return fail(SBO_EINVAL, "bad polar shape");
   const bool smem = polar_smem_bytes(p) <= kSmemBudget;
   if (!smem && ws_bytes < sbo_polar_workspace_bytes(K, p))
     return fail(SBO_EINVAL, "polar workspace too small");
   const size_t dyn = smem ? polar_smem_bytes(p) : 0;
-  cudaFuncSetAttribute(k_polar, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
-  k_polar<<<K, kJacobiThreads, dyn, as_stream(stream)>>>(P, p, counts, Q, sigma, status,
-                                                         static_cast<double*>(ws), smem ? 1 : 0);
+  if (smem) {
+    cudaFuncSetAttribute(k_polar<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(dyn));
+    k_polar<true><<<K, kJacobiThreads, dyn, as_stream(stream)>>>(
+        P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), 1);
+  } else {
+    k_polar<false><<<K, kJacobiThreads, 0, as_stream(stream)>>>(
+        P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), 0);
+  }
   return check_launch("k_polar");
 }
 
@@ -383,10 +496,15 @@ extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const doubl
   if (!smem && ws_bytes < sbo_init_workspace_bytes(p))
     return fail(SBO_EINVAL, "init workspace too small");
   const size_t dyn = smem ? init_smem_bytes(p) : 0;
-  cudaFuncSetAttribute(k_init_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(dyn));
-  k_init_block<<<1, kJacobiThreads, dyn, as_stream(stream)>>>(
-      G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), smem ? 1 : 0);
+  if (smem) {
+    cudaFuncSetAttribute(k_init_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(dyn));
+    k_init_block<true><<<1, kJacobiThreads, dyn, as_stream(stream)>>>(
+        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
+  } else {
+    k_init_block<false><<<1, kJacobiThreads, 0, as_stream(stream)>>>(
+        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 0);
+  }
   return check_launch("k_init_block");
 }
 

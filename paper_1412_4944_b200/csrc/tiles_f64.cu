@@ -12,6 +12,7 @@
 // coefficient i is kept iff fewer than k coefficients beat it under the key
 // (|c| descending, index ascending) — the stable-argsort rule of onb.py:73.
 #include "common.cuh"
+#include "topk.cuh"
 
 namespace sbo {
 
@@ -28,7 +29,7 @@ struct TileLayout {
     q_off = y_off + sizeof(double) * 64 * kSyLd;
     rows_off = q_off + sizeof(double) * 64 * 64;
     misc_off = rows_off + sizeof(int64_t) * kTile;
-    bytes = misc_off + sizeof(double) * kTile * 3 + sizeof(int) * kTile + 64;
+    bytes = misc_off + sizeof(double) * kTile * 3 + 2 * sizeof(int) * kTile + 64;
   }
 };
 
@@ -136,13 +137,92 @@ __device__ RowPick pick_row(const double* Cs, int p, int k, int kind) {
   return r;
 }
 
+// Fast exact selection for p <= 64, k <= 15: four lanes per signal (a quad);
+// lane q owns coefficients i = q + 4u, u < 16.  The fp32 magnitudes are a
+// monotone rounding of the float64 ones, so when the k-th and (k+1)-th largest
+// fp32 magnitudes differ, the kept set is exactly {i : fp32|c_i| >= t_k} — the
+// same set as the float64 stable-argsort rule.  Otherwise ok = false and the
+// caller re-decides that signal with pick_row.  All 32 lanes must call this.
+struct QuadPick {
+  bool ok;
+  uint32_t mask;  // bit u: coefficient q + 4u kept
+  double score, rest_sq;
+};
+
+__device__ __forceinline__ double quad_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+__device__ QuadPick quad_pick(const double* Cs, int p, int k, int kind, bool active) {
+  const int q = threadIdx.x & 3;
+  double c[16];
+  float a[16], srt[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int i = q + 4 * u;
+    const bool on = active && i < p;
+    c[u] = on ? Cs[i] : 0.0;
+    a[u] = on ? static_cast<float>(fabs(c[u])) : -1.0f;
+    srt[u] = a[u];
+  }
+  topk::sort_desc<16>(srt);
+#pragma unroll
+  for (int x = 1; x <= 2; x <<= 1) {
+    float other[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) other[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
+    topk::merge_top<16>(srt, other);
+  }
+  float tk = srt[0], tk1 = srt[1];
+#pragma unroll
+  for (int u = 1; u < 16; ++u) {
+    if (u == k - 1) tk = srt[u];
+    if (u == k) tk1 = srt[u];
+  }
+  QuadPick r;
+  r.ok = tk > tk1;
+  r.mask = 0u;
+  double sq = 0.0, sa = 0.0, rest = 0.0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    if (q + 4 * u < p) {
+      if (a[u] >= tk) {
+        r.mask |= 1u << u;
+        sq = fma(c[u], c[u], sq);
+        sa += fabs(c[u]);
+      } else {
+        rest = fma(c[u], c[u], rest);
+      }
+    }
+  }
+  sq = quad_sum(sq);
+  sa = quad_sum(sa);
+  r.rest_sq = quad_sum(rest);
+  r.score = kind == SBO_KIND_SQUARED_SUM ? sq : sa;
+  return r;
+}
+
+// ascending position of kept coefficient i among the quad's kept set
+__device__ __forceinline__ int quad_position(const uint32_t (&masks)[4], int i) {
+  int pos = 0;
+#pragma unroll
+  for (int q2 = 0; q2 < 4; ++q2) {
+    const int below = i > q2 ? (i - q2 + 3) >> 2 : 0;  // u' with q2 + 4u' < i
+    pos += __popc(masks[q2] & ((below >= 32) ? 0xffffffffu : ((1u << below) - 1u)));
+  }
+  return pos;
+}
+
 // ---------------------------------------------------------------------------
 // energy pass (sbo.py:177-194), fresh or incremental
 // ---------------------------------------------------------------------------
 template <typename TY>
 __global__ void __launch_bounds__(kThreads) k_energy_f64(
     const TY* __restrict__ y, int64_t m, int p, const double* __restrict__ blocks, int b0,
-    int b1, int k, int kind, int accumulate, int32_t* best, double* score, double* rest_sq,
+    int b1, int k, int kind, int accumulate, const int32_t* __restrict__ list,
+    const int32_t* __restrict__ nlist, int32_t* best, double* score, double* rest_sq,
     double* norm_sq) {
   extern __shared__ __align__(16) unsigned char smem[];
   const TileLayout L(p);
@@ -154,55 +234,75 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
   double* brest = bscore + kTile;
   double* bnorm = brest + kTile;
   int* bbest = reinterpret_cast<int*>(bnorm + kTile);
-
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kTile) {
-    const int64_t j = base + threadIdx.x;
-    rows[threadIdx.x] = j < m ? j : -1;
-    if (accumulate && j < m) {
-      bbest[threadIdx.x] = best[j];
-      bscore[threadIdx.x] = score[j];
-      brest[threadIdx.x] = rest_sq[j];
-    } else {
-      bbest[threadIdx.x] = -1;
-      bscore[threadIdx.x] = -1.0;
-      brest[threadIdx.x] = 0.0;
-    }
-  }
-  __syncthreads();
-  for (int b = b0; b < b1; ++b) {
-    project_tile(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
-    for (int s = warp; s < kTile; s += kThreads / 32) {
-      if (rows[s] < 0) continue;
-      const RowPick r = pick_row(C + s * L.ldc, p, k, kind);
-      if (lane == 0 && r.score > bscore[s]) {  // strict: first maximum wins (sbo.py:191)
-        bscore[s] = r.score;
-        brest[s] = r.rest_sq;
-        bbest[s] = b;
+  // signals: [0, m), or list[0 .. *nlist) (the float64 re-decision of flagged signals)
+  const int64_t count = list ? static_cast<int64_t>(*nlist) : m;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kTile; base < count;
+       base += static_cast<int64_t>(gridDim.x) * kTile) {
+    __syncthreads();
+    if (threadIdx.x < kTile) {
+      const int64_t t = base + threadIdx.x;
+      const int64_t j = t < count ? (list ? static_cast<int64_t>(list[t]) : t) : -1;
+      rows[threadIdx.x] = j;
+      if (accumulate && j >= 0) {
+        bbest[threadIdx.x] = best[j];
+        bscore[threadIdx.x] = score[j];
+        brest[threadIdx.x] = rest_sq[j];
+      } else {
+        bbest[threadIdx.x] = -1;
+        bscore[threadIdx.x] = -1.0;
+        brest[threadIdx.x] = 0.0;
       }
     }
     __syncthreads();
-  }
-  // ||y||^2 in float64
-  for (int s = warp; s < kTile; s += kThreads / 32) {
-    const int64_t j = rows[s];
-    if (j < 0) continue;
-    double acc = 0.0;
-    for (int kk = lane; kk < p; kk += 32) {
-      const double v = y[j * p + kk];
-      acc = fma(v, v, acc);
+    int* fb = bbest + kTile;  // per-signal "needs the exact rank method" marks
+    for (int b = b0; b < b1; ++b) {
+      project_tile(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
+      if (p <= 64 && k < 16) {
+        const int s = threadIdx.x >> 2;
+        const bool act = rows[s] >= 0;
+        const QuadPick r = quad_pick(C + s * L.ldc, p, k, kind, act);
+        if ((threadIdx.x & 3) == 0) {
+          fb[s] = act && !r.ok;
+          if (act && r.ok && r.score > bscore[s]) {  // strict: first maximum wins (sbo.py:191)
+            bscore[s] = r.score;
+            brest[s] = r.rest_sq;
+            bbest[s] = b;
+          }
+        }
+        __syncthreads();
+      }
+      for (int s = warp; s < kTile; s += kThreads / 32) {
+        if (rows[s] < 0 || (p <= 64 && k < 16 && !fb[s])) continue;
+        const RowPick r = pick_row(C + s * L.ldc, p, k, kind);
+        if (lane == 0 && r.score > bscore[s]) {
+          bscore[s] = r.score;
+          brest[s] = r.rest_sq;
+          bbest[s] = b;
+        }
+      }
+      __syncthreads();
     }
-    acc = warp_sum(acc);
-    if (lane == 0) bnorm[s] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x < kTile && rows[threadIdx.x] >= 0) {
-    const int64_t j = rows[threadIdx.x];
-    best[j] = bbest[threadIdx.x];
-    score[j] = bscore[threadIdx.x];
-    rest_sq[j] = brest[threadIdx.x];
-    if (norm_sq) norm_sq[j] = bnorm[threadIdx.x];
+    // ||y||^2 in float64
+    for (int s = warp; s < kTile; s += kThreads / 32) {
+      const int64_t j = rows[s];
+      if (j < 0) continue;
+      double acc = 0.0;
+      for (int kk = lane; kk < p; kk += 32) {
+        const double v = y[j * p + kk];
+        acc = fma(v, v, acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) bnorm[s] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < kTile && rows[threadIdx.x] >= 0) {
+      const int64_t j = rows[threadIdx.x];
+      best[j] = bbest[threadIdx.x];
+      score[j] = bscore[threadIdx.x];
+      rest_sq[j] = brest[threadIdx.x];
+      if (norm_sq) norm_sq[j] = bnorm[threadIdx.x];
+    }
   }
 }
 
@@ -238,8 +338,38 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
     }
     __syncthreads();
     project_tile(y, p, rows, q, C, L.ldc, sY, sQ);
+    int* fb = reinterpret_cast<int*>(smem + L.misc_off);
+    const bool quad = p <= 64 && k < 16;
+    if (quad) {
+      const int s = threadIdx.x >> 2, qd = threadIdx.x & 3;
+      const bool act = rows[s] >= 0;
+      const double* Cs = C + s * L.ldc;
+      const QuadPick r = quad_pick(Cs, p, k, kind, act);
+      uint32_t masks[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        masks[x] = __shfl_sync(0xffffffffu, r.mask, (threadIdx.x & 31 & ~3) | x);
+      if (qd == 0) fb[s] = act && !r.ok;
+      if (act && r.ok) {
+        const int64_t col = out_by_signal ? rows[s] : (t0 + s);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if ((r.mask >> u) & 1u) {
+            const int i = qd + 4 * u;
+            const int at = quad_position(masks, i);
+            idx[at * ld + col] = static_cast<int16_t>(i);
+            val[at * ld + col] = Cs[i];
+          }
+        }
+        if (qd == 0) {
+          if (energy) energy[col] = r.score;
+          if (rest_sq) rest_sq[col] = r.rest_sq;
+        }
+      }
+      __syncthreads();
+    }
     for (int s = warp; s < kTile; s += kThreads / 32) {
-      if (rows[s] < 0) continue;
+      if (rows[s] < 0 || (quad && !fb[s])) continue;
       const double* Cs = C + s * L.ldc;
       const RowPick r = pick_row(Cs, p, k, kind);
       const int64_t col = out_by_signal ? rows[s] : (t0 + s);
@@ -395,14 +525,18 @@ using namespace sbo;
 namespace {
 template <typename TY>
 int energy_impl(const void* yv, int64_t m, int p, const double* blocks, int b0, int b1, int k,
-                int kind, int accumulate, int32_t* best, double* score, double* rest_sq,
+                int kind, int accumulate, const int32_t* list, const int32_t* nlist,
+                int64_t max_list, int32_t* best, double* score, double* rest_sq,
                 double* norm_sq, cudaStream_t st) {
   const TileLayout L(p);
   cudaFuncSetAttribute(k_energy_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
-  k_energy_f64<TY><<<static_cast<unsigned>(ceil_div(m, kTile)), kThreads, L.bytes, st>>>(
-      static_cast<const TY*>(yv), m, p, blocks, b0, b1, k, kind, accumulate, best, score,
-      rest_sq, norm_sq);
+  int64_t tiles = ceil_div(list ? max_list : m, kTile);
+  if (list && tiles > 1184) tiles = 1184;  // grid-stride over the (device-sized) list
+  if (tiles < 1) tiles = 1;
+  k_energy_f64<TY><<<static_cast<unsigned>(tiles), kThreads, L.bytes, st>>>(
+      static_cast<const TY*>(yv), m, p, blocks, b0, b1, k, kind, accumulate, list, nlist, best,
+      score, rest_sq, norm_sq);
   return check_launch("k_energy_f64");
 }
 
@@ -452,10 +586,26 @@ extern "C" int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const
   if (m == 0 || b1 == b0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32
-             ? energy_impl<float>(y, m, p, blocks, b0, b1, k, kind, accumulate, best, score,
-                                  rest_sq, norm_sq, as_stream(stream))
-             : energy_impl<double>(y, m, p, blocks, b0, b1, k, kind, accumulate, best, score,
-                                   rest_sq, norm_sq, as_stream(stream));
+             ? energy_impl<float>(y, m, p, blocks, b0, b1, k, kind, accumulate, nullptr,
+                                  nullptr, 0, best, score, rest_sq, norm_sq, as_stream(stream))
+             : energy_impl<double>(y, m, p, blocks, b0, b1, k, kind, accumulate, nullptr,
+                                   nullptr, 0, best, score, rest_sq, norm_sq, as_stream(stream));
+}
+
+extern "C" int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p,
+                                  const double* blocks, int K, int s0, int kind,
+                                  const int32_t* list, const int32_t* nlist, int64_t max_list,
+                                  int32_t* best, double* score, double* residual_sq,
+                                  void* stream) {
+  if (int rc = check_common(dtype, p, s0)) return rc;
+  if (K < 1 || !list || !nlist) return fail(SBO_EINVAL, "recheck needs K >= 1 and a list");
+  if (max_list <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? energy_impl<float>(y, m, p, blocks, 0, K, k, kind, 0, list, nlist, max_list,
+                                  best, score, residual_sq, nullptr, as_stream(stream))
+             : energy_impl<double>(y, m, p, blocks, 0, K, k, kind, 0, list, nlist, max_list,
+                                   best, score, residual_sq, nullptr, as_stream(stream));
 }
 
 extern "C" int sbo_code_segments(const void* y, int dtype, int p, const int32_t* order,

@@ -1,0 +1,73 @@
+// Register-resident selection networks for the hard-threshold step (onb.py:58-76)
+// in the tensor-core epilogues.  All indices are compile-time constants, so the
+// arrays stay in registers; every comparator is one FMNMX pair.
+#pragma once
+
+namespace sbo {
+namespace topk {
+
+// compare-exchange so that v[i] >= v[j]
+__device__ __forceinline__ void cx(float& a, float& b) {
+  const float hi = fmaxf(a, b), lo = fminf(a, b);
+  a = hi;
+  b = lo;
+}
+
+// a bitonic sequence of N -> sorted descending
+template <int N>
+__device__ __forceinline__ void merge_desc(float* v) {
+#pragma unroll
+  for (int half = N / 2; half >= 1; half >>= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((i & half) == 0) cx(v[i], v[i + half]);
+    }
+  }
+}
+
+// any N (power of two) -> sorted descending (bitonic sort)
+template <int N>
+__device__ __forceinline__ void sort_desc(float* v) {
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int half = size / 2; half >= 1; half >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int j = i ^ half;
+        if (j > i) {
+          // descending inside even `size`-blocks, ascending inside odd ones,
+          // except the final pass which is all descending
+          const bool desc = (size == N) || ((i & size) == 0);
+          if (desc) cx(v[i], v[j]);
+          else cx(v[j], v[i]);
+        }
+      }
+    }
+  }
+}
+
+// top-G (sorted descending) of the union of two sorted-descending lists a, b;
+// result in a.  c_i = max(a_i, b_{G-1-i}) is bitonic and holds the top G.
+template <int G>
+__device__ __forceinline__ void merge_top(float* a, const float* b) {
+#pragma unroll
+  for (int i = 0; i < G; ++i) a[i] = fmaxf(a[i], b[G - 1 - i]);
+  merge_desc<G>(a);
+}
+
+// top-G of 64 values, sorted descending, into v[0..G) (v is destroyed)
+template <int G>
+__device__ __forceinline__ void top_of_64(float* v) {
+  static_assert(G >= 1 && G <= 64 && (G & (G - 1)) == 0, "G must be a power of two <= 64");
+#pragma unroll
+  for (int g = 0; g < 64; g += G) sort_desc<G>(v + g);
+#pragma unroll
+  for (int step = G; step < 64; step <<= 1) {
+#pragma unroll
+    for (int g = 0; g + step < 64; g += 2 * step) merge_top<G>(v + g, v + g + step);
+  }
+}
+
+}  // namespace topk
+}  // namespace sbo

@@ -18,6 +18,7 @@ Per iteration (K-1 blocks entering, K leaving):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,8 +26,14 @@ import torch
 
 from . import _lib as L
 
-SEG_LEN = 1024        # signals per segment of the per-block kernels
-GRAM_CHUNK = 2048     # members per Gram partial
+SEG_LEN = 1024        # max signals per segment of the per-block kernels
+FILL_CTAS = 2 * 148   # enough segments to fill every SM twice
+
+
+def seg_len(n: int) -> int:
+    """Segment length (multiple of 64, <= SEG_LEN) giving ~FILL_CTAS segments for n signals."""
+    want = -(-max(n, 1) // FILL_CTAS)
+    return int(min(SEG_LEN, max(64, -(-want // 64) * 64)))
 
 
 def _ptr(t) -> int | None:
@@ -173,15 +180,34 @@ class Engine:
         self.m_total = self.m if m_total is None else int(m_total)
         self.k_cap = int(k_cap)
         self.blocks = torch.zeros((self.k_cap, self.p, self.p), dtype=torch.float64, device=self.dev)
+        # right singular vectors of each block's last Procrustes matrix (warm start)
+        self.V = torch.empty_like(self.blocks)
         self.K = 0
         self.scratch = Scratch(self.dev)
         f64 = dict(dtype=torch.float64, device=self.dev)
         self.state = State(torch.zeros(self.m, dtype=torch.int32, device=self.dev),
                            torch.zeros(self.m, **f64), torch.zeros(self.m, **f64),
                            torch.zeros(self.m, **f64), torch.zeros(1, **f64))
-        self.idx = torch.empty((self.k, max(self.m, 1)), dtype=torch.int16, device=self.dev)
-        self.val = torch.empty((self.k, max(self.m, 1)), **f64)
         self.launches = 0
+        self.flag_counts = []
+        # tensor-core representation (p = 64): split-fp16 operands, built once
+        self.tc = self.p == 64 and os.environ.get("SBO_TC", "1") != "0" and self.m > 0
+        if self.tc:
+            mp = L.size("sbo_tc_padded_rows", self.m)
+            self.yh = torch.zeros((mp, 64), dtype=torch.float16, device=self.dev)
+            self.yl = torch.zeros((mp, 64), dtype=torch.float16, device=self.dev)
+            self.escale = torch.zeros(mp, dtype=torch.int16, device=self.dev)
+            self.flags = torch.empty(self.m, dtype=torch.int32, device=self.dev)
+            self.nflag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self._alloc_tc_blocks(self.k_cap)
+            self._call("sbo_tc_split_signals", self.sig.y.data_ptr(), self.sig.code, self.m,
+                       self.p, self.yh.data_ptr(), self.yl.data_ptr(), self.escale.data_ptr(),
+                       self.stream)
+
+    def _alloc_tc_blocks(self, cap: int):
+        self.qh = torch.zeros((cap, 64, 64), dtype=torch.float16, device=self.dev)
+        self.ql = torch.zeros((cap, 64, 64), dtype=torch.float16, device=self.dev)
+        self.fscale = torch.zeros(cap, dtype=torch.int16, device=self.dev)
 
     # ------------------------------------------------------------------ utils
     @property
@@ -198,13 +224,26 @@ class Engine:
         t = torch.as_tensor(np.asarray(blocks) if not torch.is_tensor(blocks) else blocks,
                             dtype=torch.float64)
         K = t.shape[0]
-        if K > self.k_cap:
-            grown = torch.zeros((K, self.p, self.p), dtype=torch.float64, device=self.dev)
-            self.blocks, self.k_cap = grown, K
+        self.K = 0
+        self.ensure_capacity(K)
         self.blocks[:K].copy_(t.to(self.dev))
+        self.reset_rotation(0, K)
         self.K = K
 
+    def reset_rotation(self, b0: int, b1: int):
+        """Identity warm start for the polar Jacobi of blocks [b0, b1)."""
+        self.V[b0:b1].copy_(torch.eye(self.p, dtype=torch.float64, device=self.dev).expand(
+            b1 - b0, self.p, self.p))
+
+    def v_ptr(self, b: int) -> int:
+        return self.V.data_ptr() + b * self.p * self.p * 8
+
     def ensure_capacity(self, K: int):
+        if K > self.V.shape[0]:
+            V = torch.empty((K, self.p, self.p), dtype=torch.float64, device=self.dev)
+            V[: self.V.shape[0]].copy_(self.V)
+            self.V = V
+            self.reset_rotation(self.K, K)
         if K > self.k_cap:
             grown = torch.zeros((K, self.p, self.p), dtype=torch.float64, device=self.dev)
             grown[: self.K].copy_(self.blocks[: self.K])
@@ -216,6 +255,26 @@ class Engine:
     # ------------------------------------------------------ representation
     def energy(self, b0: int, b1: int, accumulate: bool):
         s = self.state
+        if self.tc:
+            # tensor-core pass over [b0, b1), then exact float64 re-decision of
+            # the signals whose certificate failed (near-ties)
+            if self.qh.shape[0] < self.k_cap:
+                self._alloc_tc_blocks(self.k_cap)
+            self._call("sbo_tc_split_blocks", self.blocks.data_ptr(), b1, self.p,
+                       self.qh.data_ptr(), self.ql.data_ptr(), self.fscale.data_ptr(),
+                       self.stream)
+            self.nflag.zero_()
+            self._call("sbo_tc_energy", self.yh.data_ptr(), self.yl.data_ptr(),
+                       self.escale.data_ptr(), self.m, self.qh.data_ptr(), self.ql.data_ptr(),
+                       self.fscale.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
+                       s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
+                       self.flags.data_ptr(), self.nflag.data_ptr(), self.stream)
+            self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
+                       self.p, self.blocks.data_ptr(), b1, self.s0, self.kind,
+                       self.flags.data_ptr(), self.nflag.data_ptr(), self.m, s.best.data_ptr(),
+                       s.score.data_ptr(), s.residual.data_ptr(), self.stream)
+            self.flag_counts.append(self.nflag.clone())
+            return
         self._call("sbo_energy_pass", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
                    self.blocks.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
                    s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
@@ -229,7 +288,8 @@ class Engine:
                    ws.numel(), self.stream)
 
     def group(self, K: int) -> Groups:
-        max_seg = L.size("sbo_max_segments", self.m, K, SEG_LEN)
+        sl = seg_len(self.m)
+        max_seg = L.size("sbo_max_segments", self.m, K, sl)
         d = self.dev
         g = Groups(torch.empty(max(self.m, 1), dtype=torch.int32, device=d),
                    torch.empty(K + 1, dtype=torch.int64, device=d),
@@ -238,7 +298,7 @@ class Engine:
                    torch.empty(max_seg, dtype=torch.int64, device=d),
                    torch.zeros(1, dtype=torch.int32, device=d), max_seg)
         ws = self.scratch.get("group", L.size("sbo_group_workspace_bytes", self.m, K))
-        self._call("sbo_group", self.state.best.data_ptr(), self.m, K, SEG_LEN,
+        self._call("sbo_group", self.state.best.data_ptr(), self.m, K, sl,
                    g.perm.data_ptr(), g.bounds.data_ptr(), g.seg_block.data_ptr(),
                    g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(), ws.data_ptr(),
                    ws.numel(), self.stream)
@@ -246,9 +306,10 @@ class Engine:
 
     def list_segments(self, n: int) -> Groups:
         """Segment table of a single list of n entries (a member list)."""
-        nseg = max(1, math.ceil(n / SEG_LEN)) if n > 0 else 0
-        lo = torch.arange(0, max(n, 1), SEG_LEN, dtype=torch.int64, device=self.dev)[:nseg]
-        hi = torch.clamp(lo + SEG_LEN, max=n)
+        sl = seg_len(n)
+        nseg = max(1, math.ceil(n / sl)) if n > 0 else 0
+        lo = torch.arange(0, max(n, 1), sl, dtype=torch.int64, device=self.dev)[:nseg]
+        hi = torch.clamp(lo + sl, max=n)
         return Groups(None, None, torch.zeros(max(nseg, 1), dtype=torch.int32, device=self.dev),
                       lo, hi, torch.tensor([nseg], dtype=torch.int32, device=self.dev),
                       max(nseg, 1))
@@ -286,17 +347,19 @@ class Engine:
                        g.max_seg, nblocks, p, Pt.data_ptr(), self.stream)
             self.comm.allreduce(Pt)
             self._call("sbo_polar", Pt.data_ptr(), nblocks, p, _ptr(counts),
-                       self.block_ptr(first_block), None, status[r].data_ptr(),
-                       pol_ws.data_ptr(), pol_ws.numel(), self.stream)
+                       self.block_ptr(first_block), self.v_ptr(first_block), None,
+                       status[r].data_ptr(), pol_ws.data_ptr(), pol_ws.numel(), self.stream)
 
     def gram(self, members, w: int) -> torch.Tensor:
         G = torch.empty((self.p, self.p), dtype=torch.float64, device=self.dev)
-        ws = self.scratch.get("gram", L.size("sbo_gram_workspace_bytes", w, GRAM_CHUNK, self.p))
+        chunk = seg_len(w)
+        ws = self.scratch.get("gram", L.size("sbo_gram_workspace_bytes", w, chunk, self.p))
         self._call("sbo_gram", self.sig.y.data_ptr(), self.sig.code, self.p, _ptr(members), w,
-                   GRAM_CHUNK, G.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
+                   chunk, G.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
         return G
 
     def init_block(self, G, ncols: int, draws: np.ndarray, slot: int, status, rank=None):
+        self.reset_rotation(slot, slot + 1)
         d = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).to(self.dev)
         ws = self.scratch.get("init", L.size("sbo_init_workspace_bytes", self.p))
         self._call("sbo_init_block", G.data_ptr(), self.p, ncols, d.data_ptr(), d.shape[0],
@@ -317,7 +380,17 @@ class Engine:
 
     # ----------------------------------------------------------- iteration
     def represent_full(self):
+        """Full representation: winners, then exact float64 squared residuals."""
         self.energy(0, self.K, False)
+        if self.tc:
+            # the tensor-core pass certifies the winner; its residual is only
+            # float32-accurate, so recode every signal in its winning block in
+            # float64 (exact support + discarded energy), as the worst set needs
+            g = self.group(self.K)
+            ld = max(self.m, 1)
+            idx = self.scratch.get("rep_idx", 2 * self.k * ld).view(torch.int16)
+            val = self.scratch.get("rep_val", 8 * self.k * ld).view(torch.float64)
+            self.code(g.perm, g, -1, True, ld, idx, val, None, self.state.residual)
         self.residual()
 
     def rmse(self) -> float:
@@ -336,6 +409,7 @@ class Engine:
         mark()
         K0 = self.K
         self.ensure_capacity(K0 + 1)
+        self.reset_rotation(K0, K0 + 1)
         st = torch.zeros((2, rounds + 1, K0 + 1), dtype=torch.int32, device=self.dev)
         # worst set and the new block (sbo.py:353-357)
         members, n = self.worst(w)
@@ -365,6 +439,7 @@ class Engine:
         rmse = self.rmse()
         stc = st.cpu().numpy()
         cnt = counts.cpu().numpy()
+        self.last_sweeps = stc >> 8  # Jacobi sweeps per (phase, round, block)
         check_status(stc)
         empty = [b for b in range(self.K) if cnt[b] == 0]
         return IterationOut(self.K, rmse, empty, members[:n])
@@ -373,6 +448,7 @@ class Engine:
 def check_status(st: np.ndarray):
     from .linalg import DecompositionError
     from .onb import NumericalError
+    st = np.asarray(st) & 0xFF  # bits 8.. carry the Jacobi sweep count
     if (st == L.ST_NOCONV).any():
         raise DecompositionError("Jacobi SVD did not converge for a block update")
     if (st == L.ST_DEFECT).any():

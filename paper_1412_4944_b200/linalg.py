@@ -82,9 +82,9 @@ def procrustes_polar(p_mat: np.ndarray) -> np.ndarray:
     Q = torch.empty((p, p), dtype=torch.float64, device=dev)
     st = torch.zeros(1, dtype=torch.int32, device=dev)
     ws = torch.empty(L.size("sbo_polar_workspace_bytes", 1, p), dtype=torch.uint8, device=dev)
-    L.call("sbo_polar", P.data_ptr(), 1, p, None, Q.data_ptr(), None, st.data_ptr(),
+    L.call("sbo_polar", P.data_ptr(), 1, p, None, Q.data_ptr(), None, None, st.data_ptr(),
            ws.data_ptr(), ws.numel(), _stream(dev))
-    if int(st.item()) == L.ST_NOCONV:
+    if int(st.item()) & 0xFF == L.ST_NOCONV:
         raise DecompositionError(f"SVD did not converge for a {p}x{p} matrix")
     return Q.cpu().numpy()
 

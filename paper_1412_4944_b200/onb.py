@@ -108,7 +108,7 @@ def init_onb(ysub: np.ndarray, rng: np.random.Generator | None = None) -> np.nda
     st = torch.zeros(1, dtype=torch.int32, device=dev)
     rank = torch.zeros(2, dtype=torch.int32, device=dev)
     eng.init_block(G, t, draws, 0, st, rank)
-    status, used = int(st.item()), int(rank[1].item())
+    status, used = int(st.item()) & 0xFF, int(rank[1].item())
     if status == L.ST_NOCONV:
         raise DecompositionError(f"SVD did not converge for a {p}x{t} matrix")
     if used:
