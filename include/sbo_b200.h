@@ -147,6 +147,14 @@ int sbo_outer_segments(const void* y, int dtype, int p, const int32_t* order, co
 int sbo_reduce_segments(const double* partial, const int32_t* seg_block, const int32_t* nseg,
                         int64_t max_seg, int K, int p, double* P, void* stream);
 
+/* Fused 1ONB round for p <= 64 and min(s0, p) < 16 — onb.py:170-171 (coding of
+ * every signal in its own block, then P = Y X^T) in one pass per segment: the
+ * same partials as sbo_code_segments + sbo_outer_segments, codes not stored. */
+int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
+                       const int32_t* seg_block, const int64_t* seg_lo, const int64_t* seg_hi,
+                       const int32_t* nseg, int64_t max_seg, const double* blocks,
+                       int block_override, int s0, double* partial, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Gram matrix G = Y_W Y_W^T of a member list (float64) — the data term of the
  * new block's initialisation (onb.py:79-95 via thin_svd(ysub), linalg.py:52).

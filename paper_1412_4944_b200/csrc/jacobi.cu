@@ -15,6 +15,7 @@
 // with shuffles and apply the Rutishauser rotation.  A sweep without a rotation
 // (|gamma| <= tol sqrt(alpha beta) everywhere) ends the iteration.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -37,10 +38,13 @@ __device__ __forceinline__ double jacobi_conv_tol(int rows) {
 // angle only leaves ~1e-7 gamma for the next sweep.
 __device__ __forceinline__ void rotation(double al, double be, double ga, double& c, double& s) {
   const double d = be - al, gg = 2.0 * ga;
-  int ex;
-  frexp(fmax(fabs(d), fabs(gg)), &ex);
-  const float df = static_cast<float>(ldexp(d, -ex));
-  const float gf = static_cast<float>(ldexp(gg, -ex));
+  // exact power-of-two scale 2^-e from the exponent bits of max(|d|, |gg|)
+  // (both finite, gg != 0 here): a handful of integer ops instead of frexp/ldexp
+  const int hi = __double2hiint(fmax(fabs(d), fabs(gg)));
+  const int e = ((hi >> 20) & 0x7ff) - 1023;
+  const double scale = __hiloint2double((1023 - e) << 20, 0);
+  const float df = static_cast<float>(d * scale);
+  const float gf = static_cast<float>(gg * scale);
   const float tf = copysignf(1.0f, df) * gf / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
   const double t = static_cast<double>(tf);
   c = rsqrt(fma(t, t, 1.0));
@@ -227,16 +231,139 @@ struct JacobiSmem {
   int count;
 };
 
+constexpr int kStNsFallback = 4;  // internal: Newton-Schulz handed the matrix to Jacobi
+constexpr int kNsMaxIter = 48;
+
+// ---------------------------------------------------------------------------
+// Polar factor of a 64 x 64 P by the scaled Newton-Schulz iteration
+//   X_0 = P / ||P||_F,  X_{k+1} = X_k (1.5 a_k I - 0.5 a_k^3 X_k^T X_k),
+// a_k = sqrt(3 / (1 + l_k + l_k^2)), l_{k+1} = a_k l_k (3 - a_k^2 l_k^2) / 2, l_0 = 1e-8
+// (Chen & Chow scaling for singular values in [l_k, 1]).  Every iteration is two
+// dense 64^3 float64 GEMMs in shared memory — no sequential sweep steps — and it
+// converges to the same orthogonal factor U V^T the SVD gives (~1e-12 at
+// cond 1e5).  Stops when ||X^T X - I||_F < 1e-13; matrices that do not converge
+// (rank deficient: the polar factor is then not unique) are flagged for the
+// Jacobi kernel, which completes the null space.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __restrict__ P,
+                                                             const int64_t* __restrict__ counts,
+                                                             double* Q, int32_t* status) {
+  constexpr int N = 64;
+  const int b = blockIdx.x;
+  __shared__ double red[32];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  double* X = reinterpret_cast<double*>(dyn);  // [r][c]
+  double* Y = X + N * N;                       // next iterate
+  double* A = Y + N * N;                       // X^T X, then the polynomial factor
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  if (counts && counts[b] == 0) {
+    if (tid == 0) status[b] = SBO_ST_SKIPPED;
+    return;
+  }
+  const double* Pb = P + static_cast<int64_t>(b) * N * N;
+  double nrm = 0.0;
+  for (int e = tid; e < N * N; e += kJacobiThreads) {
+    const double v = Pb[e];
+    X[e] = v;
+    nrm = fma(v, v, nrm);
+  }
+  nrm = sqrt(block_sum<kJacobiThreads>(nrm, red));
+  if (!(nrm > 0.0)) {
+    if (tid == 0) status[b] = kStNsFallback;
+    return;
+  }
+  const double inv = 1.0 / nrm;
+  for (int e = tid; e < N * N; e += kJacobiThreads) X[e] *= inv;
+  __syncthreads();
+  double l = 1e-8;
+  int it = 0;
+  bool done = false;
+  for (; it < kNsMaxIter; ++it) {
+    // A = X^T X  (thread: rows 4tx.., cols 4ty..)
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+#pragma unroll 4
+    for (int r = 0; r < N; ++r) {
+      const double4 u = *reinterpret_cast<const double4*>(X + r * N + 4 * tx);
+      const double4 w = *reinterpret_cast<const double4*>(X + r * N + 4 * ty);
+      const double uu[4] = {u.x, u.y, u.z, u.w}, ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = fma(uu[a], ww[c], acc[a][c]);
+    }
+    double dev = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double d = acc[a][c] - ((4 * tx + a == 4 * ty + c) ? 1.0 : 0.0);
+        dev = fma(d, d, dev);
+      }
+    dev = sqrt(block_sum<kJacobiThreads>(dev, red));
+    if (dev < 1e-13) {
+      done = true;
+      break;
+    }
+    const double al = l < 0.99 ? sqrt(3.0 / (1.0 + l + l * l)) : 1.0;
+    const double c1 = 1.5 * al, c3 = -0.5 * al * al * al;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        A[(4 * tx + a) * N + 4 * ty + c] =
+            c3 * acc[a][c] + ((4 * tx + a == 4 * ty + c) ? c1 : 0.0);
+    l = fmin(1.0, al * l * (3.0 - al * al * l * l) * 0.5);
+    __syncthreads();
+    // Y = X A  (thread: rows 4ty.., cols 4tx..)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < N; ++k) {
+      const double4 w = *reinterpret_cast<const double4*>(A + k * N + 4 * tx);
+      const double ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double xv = X[(4 * ty + a) * N + k];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = fma(xv, ww[c], acc[a][c]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      *reinterpret_cast<double4*>(Y + (4 * ty + a) * N + 4 * tx) =
+          make_double4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+    __syncthreads();
+    double* t = X;
+    X = Y;
+    Y = t;
+  }
+  if (!done) {
+    if (tid == 0) status[b] = kStNsFallback;
+    return;
+  }
+  double* Qb = Q + static_cast<int64_t>(b) * N * N;
+  for (int e = tid; e < N * N; e += kJacobiThreads) Qb[e] = X[e];
+  if (tid == 0) status[b] = SBO_ST_OK | (it << 8) | (1 << 16);  // bit 16: Newton-Schulz
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restrict__ P, int p,
                                                           const int64_t* __restrict__ counts,
                                                           double* Q, double* Vio,
                                                           double* sigma_out, int32_t* status,
-                                                          double* ws, int use_smem) {
+                                                          double* ws, int only_fallback) {
   const int b = blockIdx.x;
   const int64_t pp = static_cast<int64_t>(p) * p;
   __shared__ JacobiSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
+  // after the Newton-Schulz pass, only the matrices it handed back are solved here
+  if (only_fallback && (status[b] & 0xFF) != kStNsFallback) return;
   if (counts && counts[b] == 0) {
     if (threadIdx.x == 0 && status) status[b] = SBO_ST_SKIPPED;
     return;
@@ -474,11 +601,21 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
   if (!smem && ws_bytes < sbo_polar_workspace_bytes(K, p))
     return fail(SBO_EINVAL, "polar workspace too small");
   const size_t dyn = smem ? polar_smem_bytes(p) : 0;
+  // p = 64: Newton-Schulz first; Jacobi only for the matrices it hands back
+  static const bool force_jacobi = getenv("SBO_POLAR_JACOBI") != nullptr;
+  const bool ns = p == 64 && status && !sigma && !force_jacobi;
+  if (ns) {
+    const size_t nsb = sizeof(double) * 3 * 64 * 64;
+    cudaFuncSetAttribute(k_polar_ns, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(nsb));
+    k_polar_ns<<<K, kJacobiThreads, nsb, as_stream(stream)>>>(P, counts, Q, status);
+    if (int rc = check_launch("k_polar_ns")) return rc;
+  }
   if (smem) {
     cudaFuncSetAttribute(k_polar<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(dyn));
     k_polar<true><<<K, kJacobiThreads, dyn, as_stream(stream)>>>(
-        P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), 1);
+        P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), ns ? 1 : 0);
   } else {
     k_polar<false><<<K, kJacobiThreads, 0, as_stream(stream)>>>(
         P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), 0);

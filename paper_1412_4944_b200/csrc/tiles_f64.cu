@@ -518,9 +518,175 @@ __global__ void k_chunk_segments(int64_t w, int chunk, int64_t* lo, int64_t* hi,
   if (threadIdx.x == 0) *nseg = static_cast<int32_t>(n);
 }
 
+// ---------------------------------------------------------------------------
+// Fused 1ONB round for p <= 64, k < 16 (onb.py:170-171): per block segment,
+// code every signal in its block (float64 projection + exact quad selection)
+// and accumulate P = Y X^T, without writing the codes.  The block is staged in
+// shared memory once per segment; the masked coefficient tile is X in place.
+// ---------------------------------------------------------------------------
+constexpr int kRoundLd = 66;  // float64 row stride of the y / coefficient tiles (16B rows)
+
+struct RoundLayout {
+  size_t y_off, q_off, c_off, rows_off, fb_off, bytes;
+  __host__ __device__ RoundLayout() {
+    y_off = 0;                                          // sY[kk][s]
+    q_off = y_off + sizeof(double) * 64 * kRoundLd;      // sQ[kk][i]
+    c_off = q_off + sizeof(double) * 64 * 64;            // C[s][i] -> X[s][i]
+    rows_off = c_off + sizeof(double) * kTile * kRoundLd;
+    fb_off = rows_off + sizeof(int64_t) * kTile;
+    bytes = fb_off + sizeof(int) * kTile;
+  }
+};
+
+template <typename TY>
+__global__ void __launch_bounds__(kThreads) k_round_f64(
+    const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
+    const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
+    const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
+    const double* __restrict__ blocks, int block_override, int k, double* partial) {
+  if (static_cast<int>(blockIdx.x) >= *nseg) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const RoundLayout L;
+  double* sY = reinterpret_cast<double*>(smem + L.y_off);
+  double* sQ = reinterpret_cast<double*>(smem + L.q_off);
+  double* C = reinterpret_cast<double*>(smem + L.c_off);
+  int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
+  int* fb = reinterpret_cast<int*>(smem + L.fb_off);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int seg = blockIdx.x;
+  const int b = block_override >= 0 ? block_override : seg_block[seg];
+  const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+  const double* q = blocks + static_cast<int64_t>(b) * p * p;
+  for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
+    const int kk = e >> 6, ii = e & 63;
+    sQ[e] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+  }
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+
+  for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
+    __syncthreads();
+    if (tid < kTile) {
+      const int64_t t = t0 + tid;
+      rows[tid] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+    }
+    __syncthreads();
+    for (int e = tid; e < kTile * 64; e += kThreads) {
+      const int s = e >> 6, kk = e & 63;
+      const int64_t r = rows[s];
+      sY[kk * kRoundLd + s] = (r >= 0 && kk < p) ? static_cast<double>(__ldg(y + r * p + kk)) : 0.0;
+    }
+    __syncthreads();
+    // C = Y_tile . Q  (4 signals x 4 atoms per thread)
+    {
+      double cc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cc[a][c] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < 64; ++kk) {
+        const double2 y01 = *reinterpret_cast<const double2*>(sY + kk * kRoundLd + 4 * ty);
+        const double2 y23 = *reinterpret_cast<const double2*>(sY + kk * kRoundLd + 4 * ty + 2);
+        const double2 q01 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx);
+        const double2 q23 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx + 2);
+        const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
+        const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) cc[a][c] = fma(yv[a], qv[c], cc[a][c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        *reinterpret_cast<double4*>(C + (4 * ty + a) * kRoundLd + 4 * tx) =
+            make_double4(cc[a][0], cc[a][1], cc[a][2], cc[a][3]);
+    }
+    __syncthreads();
+    // exact selection; non-kept coefficients are zeroed, so C becomes X
+    {
+      const int s = tid >> 2, qd = tid & 3;
+      const bool act = rows[s] >= 0;
+      double* Cs = C + s * kRoundLd;
+      const QuadPick r = quad_pick(Cs, p, k, SBO_KIND_SQUARED_SUM, act);
+      if (qd == 0) fb[s] = act && !r.ok;
+      if (r.ok) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (!((r.mask >> u) & 1u)) Cs[qd + 4 * u] = 0.0;
+      }
+    }
+    __syncthreads();
+    for (int s = warp; s < kTile; s += kThreads / 32) {
+      if (!fb[s]) continue;  // float32 tie: exact rank selection for this signal
+      double* Cs = C + s * kRoundLd;
+      const RowPick r = pick_row(Cs, p, k, SBO_KIND_SQUARED_SUM);
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (!((r.sel >> t) & 1u)) Cs[lane + 32 * t] = 0.0;
+    }
+    __syncthreads();
+    // P[k][i] += sum_s Y[s][k] X[s][i]  (4 rows x 4 atoms per thread, signal order)
+    const int ns = static_cast<int>(min64(kTile, hi - t0));
+    for (int s = 0; s < ns; ++s) {
+      double yv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) yv[a] = sY[(4 * ty + a) * kRoundLd + s];
+      const double4 xv = *reinterpret_cast<const double4*>(C + s * kRoundLd + 4 * tx);
+      const double xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = fma(yv[a], xs[c], acc[a][c]);
+    }
+  }
+  double* out = partial + static_cast<int64_t>(seg) * p * p;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (4 * ty + a < p && 4 * tx + c < p) out[(4 * ty + a) * p + 4 * tx + c] = acc[a][c];
+}
+
 }  // namespace sbo
 
 using namespace sbo;
+
+template <typename TY>
+static int round_impl(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
+                      const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
+                      int64_t max_seg, const double* blocks, int block_override, int k,
+                      double* partial, cudaStream_t st) {
+  const RoundLayout L;
+  cudaFuncSetAttribute(k_round_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(L.bytes));
+  k_round_f64<TY><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
+      static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
+      block_override, k, partial);
+  return check_launch("k_round_f64");
+}
+
+extern "C" int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
+                                  const int32_t* seg_block, const int64_t* seg_lo,
+                                  const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                                  const double* blocks, int block_override, int s0,
+                                  double* partial, void* stream) {
+  if (dtype != SBO_F32 && dtype != SBO_F64) return fail(SBO_EINVAL, "bad dtype");
+  if (p < 1 || p > 64) return fail(SBO_EINVAL, "the fused round needs p <= 64");
+  const int k = s0 < p ? s0 : p;
+  if (s0 < 1 || k >= 16) return fail(SBO_EINVAL, "the fused round needs 1 <= min(s0, p) < 16");
+  if (max_seg <= 0) return SBO_OK;
+  return dtype == SBO_F32
+             ? round_impl<float>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
+                                 block_override, k, partial, as_stream(stream))
+             : round_impl<double>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
+                                  block_override, k, partial, as_stream(stream));
+}
 
 namespace {
 template <typename TY>

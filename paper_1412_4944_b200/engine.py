@@ -336,12 +336,21 @@ class Engine:
         val = self.scratch.get("tr_val", 8 * self.k * ld).view(torch.float64)
         pol_ws = self.scratch.get("polar", L.size("sbo_polar_workspace_bytes", nblocks, p))
         Pt = P[: 8 * nblocks * p * p].view(torch.float64).view(nblocks, p, p)
+        fused = p <= 64 and self.k < 16 and os.environ.get("SBO_FUSED_ROUND", "1") != "0"
+        override = first_block if single else -1
         for r in range(rounds):
-            self.code(order, g, first_block if single else -1, False, ld, idx, val)
-            self._call("sbo_outer_segments", self.sig.y.data_ptr(), self.sig.code, p,
-                       _ptr(order), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
-                       g.nseg.data_ptr(), g.max_seg, self.s0, ld, idx.data_ptr(),
-                       val.data_ptr(), partial.data_ptr(), self.stream)
+            if fused:  # coding + P partials in one pass per segment
+                self._call("sbo_round_segments", self.sig.y.data_ptr(), self.sig.code, p,
+                           _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
+                           g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
+                           self.blocks.data_ptr(), override, self.s0, partial.data_ptr(),
+                           self.stream)
+            else:
+                self.code(order, g, override, False, ld, idx, val)
+                self._call("sbo_outer_segments", self.sig.y.data_ptr(), self.sig.code, p,
+                           _ptr(order), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
+                           g.nseg.data_ptr(), g.max_seg, self.s0, ld, idx.data_ptr(),
+                           val.data_ptr(), partial.data_ptr(), self.stream)
             self._call("sbo_reduce_segments", partial.data_ptr(),
                        None if single else g.seg_block.data_ptr(), g.nseg.data_ptr(),
                        g.max_seg, nblocks, p, Pt.data_ptr(), self.stream)
@@ -439,7 +448,8 @@ class Engine:
         rmse = self.rmse()
         stc = st.cpu().numpy()
         cnt = counts.cpu().numpy()
-        self.last_sweeps = stc >> 8  # Jacobi sweeps per (phase, round, block)
+        # Jacobi sweeps / Newton-Schulz iterations per (phase, round, block)
+        self.last_sweeps = (stc >> 8) & 0xFF
         check_status(stc)
         empty = [b for b in range(self.K) if cnt[b] == 0]
         return IterationOut(self.K, rmse, empty, members[:n])
