@@ -495,17 +495,31 @@ __global__ void k_reduce_segments(const double* __restrict__ partial,
   const int b = blockIdx.y;
   const int64_t pp = static_cast<int64_t>(p) * p;
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= pp) return;
   const int n = *nseg;
-  double acc = 0.0;
-  bool any = false;
-  for (int s = 0; s < n; ++s) {
-    if (seg_block ? seg_block[s] == b : b == 0) {
-      acc += partial[s * pp + e];
-      any = true;
+  // segments are sorted by block: binary-search block b's range [s0, s1)
+  int s0 = 0, s1 = n;
+  if (seg_block) {
+    int a = 0, z = n;
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (seg_block[mid] < b) a = mid + 1;
+      else z = mid;
     }
+    s0 = a;
+    z = n;
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (seg_block[mid] <= b) a = mid + 1;
+      else z = mid;
+    }
+    s1 = a;
+  } else if (b != 0) {
+    s1 = 0;
   }
-  P[b * pp + e] = any ? acc : 0.0;
+  if (e >= pp) return;
+  double acc = 0.0;
+  for (int s = s0; s < s1; ++s) acc += partial[s * pp + e];
+  P[b * pp + e] = acc;
 }
 
 // Gram partials over chunks of a member list, then the ordered reduction
@@ -539,7 +553,7 @@ struct RoundLayout {
 };
 
 template <typename TY>
-__global__ void __launch_bounds__(kThreads) k_round_f64(
+__global__ void __launch_bounds__(kThreads, 2) k_round_f64(
     const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
     const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
     const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
@@ -568,19 +582,59 @@ __global__ void __launch_bounds__(kThreads) k_round_f64(
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
 
+  // Signal tiles are staged signal-major (sY[s][k]): coalesced global loads,
+  // contiguous stores, 16-byte reads in the outer product.  The next tile's
+  // values are prefetched into registers while the current tile computes.
+  // Thread t fetches signals (t >> 4) + 16 j, coordinates 4 (t & 15) .. + 3.
+  const int c4 = tid & 15;
+  TY pre[16];
+  int64_t prow[4];
+  auto fetch = [&](int64_t base) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t t = base + (tid >> 4) + 16 * j;
+      prow[j] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = prow[j];
+      if (p == 64 && r >= 0) {
+        if constexpr (sizeof(TY) == 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(y + r * 64) + c4);
+          pre[4 * j] = v.x;
+          pre[4 * j + 1] = v.y;
+          pre[4 * j + 2] = v.z;
+          pre[4 * j + 3] = v.w;
+        } else {
+          const double2 v0 = __ldg(reinterpret_cast<const double2*>(y + r * 64) + 2 * c4);
+          const double2 v1 = __ldg(reinterpret_cast<const double2*>(y + r * 64) + 2 * c4 + 1);
+          pre[4 * j] = v0.x;
+          pre[4 * j + 1] = v0.y;
+          pre[4 * j + 2] = v1.x;
+          pre[4 * j + 3] = v1.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int kk = 4 * c4 + i;
+          pre[4 * j + i] = (r >= 0 && kk < p) ? __ldg(y + r * p + kk) : TY(0);
+        }
+      }
+    }
+  };
+  fetch(lo);
   for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
-    __syncthreads();
-    if (tid < kTile) {
-      const int64_t t = t0 + tid;
-      rows[tid] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+    __syncthreads();  // the previous tile's outer product is done with sY / C
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int s = (tid >> 4) + 16 * j;
+      *reinterpret_cast<double4*>(sY + s * kRoundLd + 4 * c4) =
+          make_double4(static_cast<double>(pre[4 * j]), static_cast<double>(pre[4 * j + 1]),
+                       static_cast<double>(pre[4 * j + 2]), static_cast<double>(pre[4 * j + 3]));
+      if (c4 == 0) rows[s] = prow[j];
     }
     __syncthreads();
-    for (int e = tid; e < kTile * 64; e += kThreads) {
-      const int s = e >> 6, kk = e & 63;
-      const int64_t r = rows[s];
-      sY[kk * kRoundLd + s] = (r >= 0 && kk < p) ? static_cast<double>(__ldg(y + r * p + kk)) : 0.0;
-    }
-    __syncthreads();
+    if (t0 + kTile < hi) fetch(t0 + kTile);  // loads in flight during this tile
     // C = Y_tile . Q  (4 signals x 4 atoms per thread)
     {
       double cc[4][4];
@@ -590,11 +644,11 @@ __global__ void __launch_bounds__(kThreads) k_round_f64(
         for (int c = 0; c < 4; ++c) cc[a][c] = 0.0;
 #pragma unroll 4
       for (int kk = 0; kk < 64; ++kk) {
-        const double2 y01 = *reinterpret_cast<const double2*>(sY + kk * kRoundLd + 4 * ty);
-        const double2 y23 = *reinterpret_cast<const double2*>(sY + kk * kRoundLd + 4 * ty + 2);
+        double yv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) yv[a] = sY[(4 * ty + a) * kRoundLd + kk];
         const double2 q01 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx);
         const double2 q23 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx + 2);
-        const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
         const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -633,12 +687,11 @@ __global__ void __launch_bounds__(kThreads) k_round_f64(
     __syncthreads();
     // P[k][i] += sum_s Y[s][k] X[s][i]  (4 rows x 4 atoms per thread, signal order)
     const int ns = static_cast<int>(min64(kTile, hi - t0));
+#pragma unroll 2
     for (int s = 0; s < ns; ++s) {
-      double yv[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) yv[a] = sY[(4 * ty + a) * kRoundLd + s];
-      const double4 xv = *reinterpret_cast<const double4*>(C + s * kRoundLd + 4 * tx);
-      const double xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      const double4 yq = *reinterpret_cast<const double4*>(sY + s * kRoundLd + 4 * ty);
+      const double4 xq = *reinterpret_cast<const double4*>(C + s * kRoundLd + 4 * tx);
+      const double yv[4] = {yq.x, yq.y, yq.z, yq.w}, xs[4] = {xq.x, xq.y, xq.z, xq.w};
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll

@@ -471,24 +471,22 @@ def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int]:
     Keys are the float64 bit patterns of residual_sq (order-preserving for >= 0);
     ties at the threshold go to the lowest GLOBAL signal index, i.e. to lower
     ranks first (contiguous column shards)."""
+    from .dist import equal_quota, select_threshold
+
     res = eng.state.residual
-    m_total = eng.m_total
-    need = min(w, m_total)
-    prefix = 0
     hist = torch.zeros(256, dtype=torch.int64, device=eng.dev)
-    for shift in range(56, -8, -8):
+
+    def local_hist(prefix: int, shift: int) -> np.ndarray:
         hist.zero_()
         eng._call("sbo_key_histogram", res.data_ptr(), eng.m, prefix, shift, hist.data_ptr(),
                   eng.stream)
-        h = eng.comm.allreduce(hist).cpu().numpy()
-        cum = 0
-        for d in range(255, -1, -1):
-            if cum + h[d] >= need:
-                break
-            cum += int(h[d])
-        need -= cum
-        prefix |= d << shift
-    # equal-key members: lowest global indices first -> lower ranks first
+        return hist.cpu().numpy()
+
+    def allreduce(h: np.ndarray) -> np.ndarray:
+        t = torch.from_numpy(h).to(eng.dev)
+        return eng.comm.allreduce(t).cpu().numpy()
+
+    prefix, need_eq = select_threshold(local_hist, allreduce, min(w, eng.m_total))
     cnt = torch.zeros(2, dtype=torch.int64, device=eng.dev)
     members = torch.empty(max(eng.m, 1), dtype=torch.int32, device=eng.dev)
     ws = eng.scratch.get("worst", L.size("sbo_worst_workspace_bytes", eng.m))
@@ -496,9 +494,7 @@ def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int]:
     eng._call("sbo_worst_collect", res.data_ptr(), eng.m, prefix, 0, members.data_ptr(),
               cnt.data_ptr(), ws.data_ptr(), ws.numel(), eng.stream)
     gt, eq = (int(x) for x in cnt.cpu().numpy())
-    eqs = eng.comm.allgather_int(eq)
-    before = sum(eqs[: eng.comm.rank])
-    take = max(0, min(eq, need - before))
+    take = equal_quota(eng.comm.allgather_int(eq), eng.comm.rank, need_eq)
     eng._call("sbo_worst_collect", res.data_ptr(), eng.m, prefix, take, members.data_ptr(),
               cnt.data_ptr(), ws.data_ptr(), ws.numel(), eng.stream)
     return members, gt + take
