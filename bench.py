@@ -117,6 +117,46 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+# Algorithmic work per unit of each timed ABI call:
+#   round  (sbo_round_segments, unit = signal):  own-block projection 2p^2 +
+#          sparse outer product 2 p k — the reference's train_onb round
+#   tc     (sbo_tc_energy, unit = signal x block): projection 2p^2
+#   code   (sbo_code_segments, unit = signal): projection 2p^2
+FP64_PEAK_TFLOPS = 33.0  # measured FFMA.F64 throughput on this pool (profiles/fp64_micro.txt)
+
+
+def kernel_families(timer, p, k):
+    fam = {"sbo_round_segments": ("k_round_f64", 2 * p * p + 2 * p * k, "fp64 CUDA cores"),
+           "sbo_tc_energy": ("k_energy_tc", 2 * p * p, "tcgen05 split-fp16"),
+           "sbo_code_segments": ("k_code_f64", 2 * p * p, "fp64 CUDA cores"),
+           "sbo_polar": ("k_polar_ns", 0, "fp64 CUDA cores (latency)"),
+           "sbo_energy_recheck": ("k_energy_f64 recheck", 0, "fp64 CUDA cores")}
+    out = {}
+    for name, (kname, fpu, pipe) in fam.items():
+        ev = [(u, e0.elapsed_time(e1)) for (n, u, e0, e1) in timer if n == name]
+        if not ev:
+            continue
+        ms = sum(t for _, t in ev)
+        units = sum(u for u, _ in ev)
+        out[kname] = {"launches": len(ev), "ms_total": ms, "units": units,
+                      "flop_per_unit": fpu, "pipe": pipe,
+                      "tflops": (fpu * units / (ms * 1e-3) / 1e12) if fpu and ms else None}
+    return out
+
+
+def roofline_of(kname, info, bf16, src, steps):
+    achieved = info["tflops"] or 0.0
+    return {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": bf16,
+            "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
+            "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
+            "fp64_peak": FP64_PEAK_TFLOPS,
+            "frac_of_fp64_peak": achieved / FP64_PEAK_TFLOPS if "fp64" in info["pipe"] else None,
+            "pipe": info["pipe"], "launches_per_step": info["launches"] / steps,
+            "ms_per_step": info["ms_total"] / steps,
+            "algorithmic": f"{info['flop_per_unit']} flop per unit, {info['units'] // steps} "
+                           "units per step (DESIGN.md)"}
+
+
 def iteration_model(p, K, s0, R, w_frac):
     """SURVEY.md §8(d) algorithmic FLOPs and bytes per signal of one iteration."""
     flops = 2 * p * p * (K + R) + 2 * p * s0 * R + w_frac * (2 * p * p * (R + 1) + 2 * p * s0 * R)
@@ -241,11 +281,12 @@ def run_ours(a):
     calls = {}
     orig = eng._call
 
-    def counting(name, *args):
+    def counting(name, *args, **kw):
         calls[name] = calls.get(name, 0) + 1
-        return orig(name, *args)
+        return orig(name, *args, **kw)
 
     eng._call = counting
+    eng.timer = []  # per-call CUDA events on the launching stream (engine._call)
     sampler = ClockSampler(local)
     marks = []
     if world > 1:
@@ -274,12 +315,12 @@ def run_ours(a):
     t_step = elapsed / a.steps
     value = m_total / t_step
     launches = sum(KERNELS_PER_CALL.get(n, 1) * c for n, c in calls.items())
-    # dominant kernel: the full energy pass of represent #2 (events inside the timed region)
-    rep2 = [mk.ev[3].elapsed_time(mk.ev[4]) / 1e3 for mk in marks]
-    t_rep2 = float(np.mean(rep2))
     hbm, bf16, src = peaks()
-    flops_energy = 2.0 * p * p * a.K * a.m
-    achieved = flops_energy / t_rep2 / 1e12
+    kernels = kernel_families(eng.timer, p, min(a.s0, p))
+    eng.timer = None
+    dom = max(kernels.items(), key=lambda kv: kv[1]["ms_total"])
+    for v in kernels.values():
+        v["ms_per_step"] = v["ms_total"] / a.steps
     f_sig, b_sig = iteration_model(p, a.K, a.s0, a.rounds, 1.0 / 16)
     t_roof = max(f_sig * a.m / (bf16 / 2 * 1e12), b_sig * a.m / (hbm * 1e9))
     phases = np.mean([[mk.ev[i].elapsed_time(mk.ev[i + 1]) for i in range(4)] for mk in marks],
@@ -317,11 +358,8 @@ def run_ours(a):
         "gpu_launches": launches,
         "phases_ms": {"worst+new_block": phases[0], "represent1": phases[1],
                       "group+retrain": phases[2], "represent2": phases[3]},
-        "roofline": {"kernel": "k_energy_f64 (represent #2 energy/argmax pass)",
-                     "bound": "tensor", "achieved": achieved, "peak": bf16,
-                     "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
-                     "peak_source": f"{src} bf16 dense (TF32 dense = peak/2)",
-                     "algorithmic": f"2*p^2*K flop/signal x {a.m} signals per launch"},
+        "roofline": roofline_of(dom[0], dom[1], bf16, src, steps=a.steps),
+        "kernels": {k: v for k, v in kernels.items() if v},
         "iteration_roofline": {"flop_per_signal": f_sig, "bytes_per_signal": b_sig,
                                "t_roof_ms": t_roof * 1e3, "frac": t_roof / t_step,
                                "model": "SURVEY.md 8(d): max(F/TF32 peak, B/HBM)"},

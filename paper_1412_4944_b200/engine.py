@@ -214,9 +214,19 @@ class Engine:
     def stream(self) -> int:
         return torch.cuda.current_stream(self.dev).cuda_stream
 
-    def _call(self, name, *args):
+    def _call(self, name, *args, units: int = 0):
+        """One ABI call.  With ``self.timer`` set (bench.py), the call is bracketed
+        by CUDA events on this stream and credited with ``units`` signals."""
         self.launches += 1
+        t = getattr(self, "timer", None)
+        if t is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         L.call(name, *args)
+        if t is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            t.append((name, units, e0, e1))
         if L.debug_sync():
             torch.cuda.synchronize(self.dev)
 
@@ -268,7 +278,8 @@ class Engine:
                        self.escale.data_ptr(), self.m, self.qh.data_ptr(), self.ql.data_ptr(),
                        self.fscale.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
                        s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
-                       self.flags.data_ptr(), self.nflag.data_ptr(), self.stream)
+                       self.flags.data_ptr(), self.nflag.data_ptr(), self.stream,
+                       units=self.m * (b1 - b0))
             self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
                        self.p, self.blocks.data_ptr(), b1, self.s0, self.kind,
                        self.flags.data_ptr(), self.nflag.data_ptr(), self.m, s.best.data_ptr(),
@@ -320,7 +331,8 @@ class Engine:
                    _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
                    g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, self.blocks.data_ptr(),
                    block_override, self.s0, self.kind, int(out_by_signal), ld,
-                   idx.data_ptr(), val.data_ptr(), _ptr(energy), _ptr(kept), self.stream)
+                   idx.data_ptr(), val.data_ptr(), _ptr(energy), _ptr(kept), self.stream,
+                   units=self.m if order is not None and g.bounds is not None else 0)
 
     # ----------------------------------------------------------- training
     def train_rounds(self, order, g: Groups, n: int, rounds: int, nblocks: int,
@@ -344,7 +356,7 @@ class Engine:
                            _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
                            g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
                            self.blocks.data_ptr(), override, self.s0, partial.data_ptr(),
-                           self.stream)
+                           self.stream, units=n)
             else:
                 self.code(order, g, override, False, ld, idx, val)
                 self._call("sbo_outer_segments", self.sig.y.data_ptr(), self.sig.code, p,
@@ -357,7 +369,8 @@ class Engine:
             self.comm.allreduce(Pt)
             self._call("sbo_polar", Pt.data_ptr(), nblocks, p, _ptr(counts),
                        self.block_ptr(first_block), self.v_ptr(first_block), None,
-                       status[r].data_ptr(), pol_ws.data_ptr(), pol_ws.numel(), self.stream)
+                       status[r].data_ptr(), pol_ws.data_ptr(), pol_ws.numel(), self.stream,
+                       units=nblocks)
 
     def gram(self, members, w: int) -> torch.Tensor:
         G = torch.empty((self.p, self.p), dtype=torch.float64, device=self.dev)
