@@ -245,17 +245,23 @@ constexpr int kNsMaxIter = 48;
 // (rank deficient: the polar factor is then not unique) are flagged for the
 // Jacobi kernel, which completes the null space.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __restrict__ P,
                                                              const int64_t* __restrict__ counts,
                                                              double* Q, int32_t* status) {
-  constexpr int N = 64;
+  constexpr int N = 64, LD = 68;  // padded rows: conflict-free DMMA fragment loads
   const int b = blockIdx.x;
   __shared__ double red[32];
   extern __shared__ __align__(16) unsigned char dyn[];
   double* X = reinterpret_cast<double*>(dyn);  // [r][c]
-  double* Y = X + N * N;                       // next iterate
-  double* A = Y + N * N;                       // X^T X, then the polynomial factor
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double* Y = X + N * LD;                      // next iterate
+  double* A = Y + N * LD;                      // polynomial factor
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   if (counts && counts[b] == 0) {
     if (tid == 0) status[b] = SBO_ST_SKIPPED;
     return;
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
   double nrm = 0.0;
   for (int e = tid; e < N * N; e += kJacobiThreads) {
     const double v = Pb[e];
-    X[e] = v;
+    X[(e >> 6) * LD + (e & 63)] = v;
     nrm = fma(v, v, nrm);
   }
   nrm = sqrt(block_sum<kJacobiThreads>(nrm, red));
@@ -273,34 +279,30 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
     return;
   }
   const double inv = 1.0 / nrm;
-  for (int e = tid; e < N * N; e += kJacobiThreads) X[e] *= inv;
+  for (int e = tid; e < N * N; e += kJacobiThreads) X[(e >> 6) * LD + (e & 63)] *= inv;
   __syncthreads();
   double l = 1e-8;
   int it = 0;
   bool done = false;
+  const int row = 8 * warp + g;  // this thread's output row in both GEMMs
   for (; it < kNsMaxIter; ++it) {
-    // A = X^T X  (thread: rows 4tx.., cols 4ty..)
-    double acc[4][4];
+    // G = X^T X on DMMA: warp w owns rows [8w, 8w+8) x 64
+    double acc[8][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+    for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
 #pragma unroll 4
-    for (int r = 0; r < N; ++r) {
-      const double4 u = *reinterpret_cast<const double4*>(X + r * N + 4 * tx);
-      const double4 w = *reinterpret_cast<const double4*>(X + r * N + 4 * ty);
-      const double uu[4] = {u.x, u.y, u.z, u.w}, ww[4] = {w.x, w.y, w.z, w.w};
+    for (int r0 = 0; r0 < N; r0 += 4) {
+      const double* xr = X + (r0 + t4) * LD;
+      const double a = xr[8 * warp + g];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = fma(uu[a], ww[c], acc[a][c]);
+      for (int n = 0; n < 8; ++n) dmma64(acc[n][0], acc[n][1], a, xr[8 * n + g]);
     }
     double dev = 0.0;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int n = 0; n < 8; ++n)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double d = acc[a][c] - ((4 * tx + a == 4 * ty + c) ? 1.0 : 0.0);
+      for (int h = 0; h < 2; ++h) {
+        const double d = acc[n][h] - ((row == 8 * n + 2 * t4 + h) ? 1.0 : 0.0);
         dev = fma(d, d, dev);
       }
     dev = sqrt(block_sum<kJacobiThreads>(dev, red));
@@ -311,33 +313,29 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
     const double al = l < 0.99 ? sqrt(3.0 / (1.0 + l + l * l)) : 1.0;
     const double c1 = 1.5 * al, c3 = -0.5 * al * al * al;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        A[(4 * tx + a) * N + 4 * ty + c] =
-            c3 * acc[a][c] + ((4 * tx + a == 4 * ty + c) ? c1 : 0.0);
+    for (int n = 0; n < 8; ++n) {
+      const int col = 8 * n + 2 * t4;
+      *reinterpret_cast<double2*>(A + row * LD + col) =
+          make_double2(c3 * acc[n][0] + (row == col ? c1 : 0.0),
+                       c3 * acc[n][1] + (row == col + 1 ? c1 : 0.0));
+    }
     l = fmin(1.0, al * l * (3.0 - al * al * l * l) * 0.5);
     __syncthreads();
-    // Y = X A  (thread: rows 4ty.., cols 4tx..)
+    // Y = X A on DMMA
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+    for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
+    const double* xa = X + row * LD + t4;
 #pragma unroll 4
-    for (int k = 0; k < N; ++k) {
-      const double4 w = *reinterpret_cast<const double4*>(A + k * N + 4 * tx);
-      const double ww[4] = {w.x, w.y, w.z, w.w};
+    for (int k0 = 0; k0 < N; k0 += 4) {
+      const double a = xa[k0];
+      const double* ab = A + (k0 + t4) * LD + g;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const double xv = X[(4 * ty + a) * N + k];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = fma(xv, ww[c], acc[a][c]);
-      }
+      for (int n = 0; n < 8; ++n) dmma64(acc[n][0], acc[n][1], a, ab[8 * n]);
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-      *reinterpret_cast<double4*>(Y + (4 * ty + a) * N + 4 * tx) =
-          make_double4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+    for (int n = 0; n < 8; ++n)
+      *reinterpret_cast<double2*>(Y + row * LD + 8 * n + 2 * t4) =
+          make_double2(acc[n][0], acc[n][1]);
     __syncthreads();
     double* t = X;
     X = Y;
@@ -348,7 +346,7 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
     return;
   }
   double* Qb = Q + static_cast<int64_t>(b) * N * N;
-  for (int e = tid; e < N * N; e += kJacobiThreads) Qb[e] = X[e];
+  for (int e = tid; e < N * N; e += kJacobiThreads) Qb[e] = X[(e >> 6) * LD + (e & 63)];
   if (tid == 0) status[b] = SBO_ST_OK | (it << 8) | (1 << 16);  // bit 16: Newton-Schulz
 }
 
@@ -605,7 +603,7 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
   static const bool force_jacobi = getenv("SBO_POLAR_JACOBI") != nullptr;
   const bool ns = p == 64 && status && !sigma && !force_jacobi;
   if (ns) {
-    const size_t nsb = sizeof(double) * 3 * 64 * 64;
+    const size_t nsb = sizeof(double) * 3 * 64 * 68;
     cudaFuncSetAttribute(k_polar_ns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(nsb));
     k_polar_ns<<<K, kJacobiThreads, nsb, as_stream(stream)>>>(P, counts, Q, status);

@@ -18,20 +18,64 @@ namespace sbo {
 
 constexpr int kSyLd = kTile + 2;  // float64 row stride of the staged y chunk (16B aligned rows)
 
+// p <= 64 tiles use the float64 tensor cores (DMMA) with 68-double rows
+constexpr int kDmmaLd = 68;
+
 struct TileLayout {
   int p, ldc;
   size_t c_off, y_off, q_off, rows_off, misc_off, bytes;
   __host__ __device__ explicit TileLayout(int p_) : p(p_) {
-    ldc = p + 1;
+    ldc = p <= 64 ? kDmmaLd : p + 1;
     c_off = 0;
     y_off = c_off + sizeof(double) * kTile * ldc;
     y_off = (y_off + 15) & ~size_t(15);
-    q_off = y_off + sizeof(double) * 64 * kSyLd;
-    rows_off = q_off + sizeof(double) * 64 * 64;
+    q_off = y_off + sizeof(double) * 64 * kDmmaLd;
+    rows_off = q_off + sizeof(double) * 64 * kDmmaLd;
     misc_off = rows_off + sizeof(int64_t) * kTile;
     bytes = misc_off + sizeof(double) * kTile * 3 + 2 * sizeof(int) * kTile + 64;
   }
 };
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// p <= 64 staging, zero padded to 64: signals signal-major sY[s][k], block sQ[k][i]
+template <typename TY>
+__device__ void stage_y64(const TY* __restrict__ y, int p, const int64_t* rows, double* sY) {
+  for (int e = threadIdx.x; e < kTile * 64; e += kThreads) {
+    const int s = e >> 6, kk = e & 63;
+    const int64_t r = rows[s];
+    sY[s * kDmmaLd + kk] = (r >= 0 && kk < p) ? static_cast<double>(__ldg(y + r * p + kk)) : 0.0;
+  }
+}
+__device__ void stage_q64(const double* __restrict__ q, int p, double* sQ) {
+  for (int e = threadIdx.x; e < 64 * 64; e += kThreads) {
+    const int kk = e >> 6, ii = e & 63;
+    sQ[kk * kDmmaLd + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+  }
+}
+// C[s][i] = sum_k sY[s][k] sQ[k][i] on DMMA; warp w: signals [8w, 8w+8) x 64 atoms
+__device__ void project64_dmma(const double* sY, const double* sQ, double* C) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  double c[8][2];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
+  const double* ya = sY + (8 * warp + g) * kDmmaLd + t4;
+#pragma unroll 4
+  for (int k0 = 0; k0 < 64; k0 += 4) {
+    const double a = ya[k0];
+    const double* qb = sQ + (k0 + t4) * kDmmaLd + g;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) dmma8(c[n][0], c[n][1], a, qb[8 * n]);
+  }
+  double* crow = C + (8 * warp + g) * kDmmaLd + 2 * t4;
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+    *reinterpret_cast<double2*>(crow + 8 * n) = make_double2(c[n][0], c[n][1]);
+}
 
 // C[s][i] = sum_k y[rows[s]][k] * Q[k][i]  (float64 FMA chain over k ascending)
 template <typename TY>
@@ -256,8 +300,17 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
     }
     __syncthreads();
     int* fb = bbest + kTile;  // per-signal "needs the exact rank method" marks
+    if (p <= 64) stage_y64(y, p, rows, sY);
     for (int b = b0; b < b1; ++b) {
-      project_tile(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
+      if (p <= 64) {
+        __syncthreads();
+        stage_q64(blocks + static_cast<int64_t>(b) * p * p, p, sQ);
+        __syncthreads();
+        project64_dmma(sY, sQ, C);
+        __syncthreads();
+      } else {
+        project_tile(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
+      }
       if (p <= 64 && k < 16) {
         const int s = threadIdx.x >> 2;
         const bool act = rows[s] >= 0;
@@ -330,6 +383,7 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
   const double* q = blocks + static_cast<int64_t>(b) * p * p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
+  if (p <= 64) stage_q64(q, p, sQ);  // the segment's block, staged once
   for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
     __syncthreads();
     if (threadIdx.x < kTile) {
@@ -337,7 +391,14 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
       rows[threadIdx.x] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
     }
     __syncthreads();
-    project_tile(y, p, rows, q, C, L.ldc, sY, sQ);
+    if (p <= 64) {
+      stage_y64(y, p, rows, sY);
+      __syncthreads();
+      project64_dmma(sY, sQ, C);
+      __syncthreads();
+    } else {
+      project_tile(y, p, rows, q, C, L.ldc, sY, sQ);
+    }
     int* fb = reinterpret_cast<int*>(smem + L.misc_off);
     const bool quad = p <= 64 && k < 16;
     if (quad) {
@@ -538,14 +599,26 @@ __global__ void k_chunk_segments(int64_t w, int chunk, int64_t* lo, int64_t* hi,
 // and accumulate P = Y X^T, without writing the codes.  The block is staged in
 // shared memory once per segment; the masked coefficient tile is X in place.
 // ---------------------------------------------------------------------------
-constexpr int kRoundLd = 66;  // float64 row stride of the y / coefficient tiles (16B rows)
+// float64 row stride of the y / block / coefficient tiles: 68 doubles keeps the
+// DMMA fragment loads (4 rows x 4-8 consecutive doubles per half-warp) free of
+// shared-memory bank conflicts and rows 16-byte aligned
+constexpr int kRoundLd = 68;
+
+// D(8x8) += A(8x4) B(4x8) on the float64 tensor cores (mma.sync m8n8k4, DMMA).
+// Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// d0/d1 = D[lane>>2][2(lane&3)], D[lane>>2][2(lane&3)+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 struct RoundLayout {
   size_t y_off, q_off, c_off, rows_off, fb_off, bytes;
   __host__ __device__ RoundLayout() {
-    y_off = 0;                                          // sY[kk][s]
+    y_off = 0;                                          // sY[s][kk]
     q_off = y_off + sizeof(double) * 64 * kRoundLd;      // sQ[kk][i]
-    c_off = q_off + sizeof(double) * 64 * 64;            // C[s][i] -> X[s][i]
+    c_off = q_off + sizeof(double) * 64 * kRoundLd;      // C[s][i] -> X[s][i]
     rows_off = c_off + sizeof(double) * kTile * kRoundLd;
     fb_off = rows_off + sizeof(int64_t) * kTile;
     bytes = fb_off + sizeof(int) * kTile;
@@ -574,13 +647,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_round_f64(
   const double* q = blocks + static_cast<int64_t>(b) * p * p;
   for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
     const int kk = e >> 6, ii = e & 63;
-    sQ[e] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+    sQ[kk * kRoundLd + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
   }
-  double acc[4][4];
+  // P accumulator: warp w owns rows [8w, 8w+8) x 64 atoms as 8 DMMA tiles
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[8][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+  for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
 
   // Signal tiles are staged signal-major (sY[s][k]): coalesced global loads,
   // contiguous stores, 16-byte reads in the outer product.  The next tile's
@@ -635,30 +708,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_round_f64(
     }
     __syncthreads();
     if (t0 + kTile < hi) fetch(t0 + kTile);  // loads in flight during this tile
-    // C = Y_tile . Q  (4 signals x 4 atoms per thread)
+    // C = Y_tile . Q on DMMA: warp w computes signals [8w, 8w+8) x 64 atoms
     {
-      double cc[4][4];
+      double c[8][2];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cc[a][c] = 0.0;
+      for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
+      const double* ya = sY + (8 * warp + g) * kRoundLd + t4;
 #pragma unroll 4
-      for (int kk = 0; kk < 64; ++kk) {
-        double yv[4];
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const double a = ya[k0];
+        const double* qb = sQ + (k0 + t4) * kRoundLd + g;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) yv[a] = sY[(4 * ty + a) * kRoundLd + kk];
-        const double2 q01 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx);
-        const double2 q23 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx + 2);
-        const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) cc[a][c] = fma(yv[a], qv[c], cc[a][c]);
+        for (int n = 0; n < 8; ++n) dmma(c[n][0], c[n][1], a, qb[8 * n]);
       }
+      double* crow = C + (8 * warp + g) * kRoundLd + 2 * t4;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-        *reinterpret_cast<double4*>(C + (4 * ty + a) * kRoundLd + 4 * tx) =
-            make_double4(cc[a][0], cc[a][1], cc[a][2], cc[a][3]);
+      for (int n = 0; n < 8; ++n)
+        *reinterpret_cast<double2*>(crow + 8 * n) = make_double2(c[n][0], c[n][1]);
     }
     __syncthreads();
     // exact selection; non-kept coefficients are zeroed, so C becomes X
@@ -685,25 +751,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_round_f64(
         if (!((r.sel >> t) & 1u)) Cs[lane + 32 * t] = 0.0;
     }
     __syncthreads();
-    // P[k][i] += sum_s Y[s][k] X[s][i]  (4 rows x 4 atoms per thread, signal order)
-    const int ns = static_cast<int>(min64(kTile, hi - t0));
-#pragma unroll 2
-    for (int s = 0; s < ns; ++s) {
-      const double4 yq = *reinterpret_cast<const double4*>(sY + s * kRoundLd + 4 * ty);
-      const double4 xq = *reinterpret_cast<const double4*>(C + s * kRoundLd + 4 * tx);
-      const double yv[4] = {yq.x, yq.y, yq.z, yq.w}, xs[4] = {xq.x, xq.y, xq.z, xq.w};
+    // P[k][i] += sum_s Y[s][k] X[s][i] on DMMA: A = Y^T, B = X, signals in order
+    // (rows beyond the tile's signals are zero in both Y and X)
+    const double* ya = sY + t4 * kRoundLd + 8 * warp + g;
+    const double* xb = C + t4 * kRoundLd + g;
+#pragma unroll 4
+    for (int s0 = 0; s0 < kTile; s0 += 4) {
+      const double a = ya[s0 * kRoundLd];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = fma(yv[a], xs[c], acc[a][c]);
+      for (int n = 0; n < 8; ++n) dmma(acc[n][0], acc[n][1], a, xb[s0 * kRoundLd + 8 * n]);
     }
   }
   double* out = partial + static_cast<int64_t>(seg) * p * p;
+  const int row = 8 * warp + g;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int n = 0; n < 8; ++n)
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (4 * ty + a < p && 4 * tx + c < p) out[(4 * ty + a) * p + 4 * tx + c] = acc[a][c];
+    for (int h = 0; h < 2; ++h) {
+      const int col = 8 * n + 2 * t4 + h;
+      if (row < p && col < p) out[row * p + col] = acc[n][h];
+    }
 }
 
 }  // namespace sbo

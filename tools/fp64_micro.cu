@@ -62,7 +62,9 @@ __global__ void bar_lat(double* out, long long* cycles, int n) {
   if (threadIdx.x == 0) cycles[0] = t1 - t0;
 }
 
+int dmma_main();
 int main() {
+  dmma_main();
   double* d;
   float* f;
   long long* cyc;
@@ -108,6 +110,47 @@ int main() {
     cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
     if (pass) printf("FP32 FMA throughput: %.1f TFLOP/s\n", 2.0 * 8 * m * sms * 4 * 256 / (ms * 1e9));
+  }
+  return 0;
+}
+
+// DMMA m8n8k4 f64 throughput (register-resident operands, 4 independent chains per warp)
+__global__ void dmma_tp(double* out, int n) {
+  double a = out[threadIdx.x & 7] + 1.0, b = out[(threadIdx.x + 3) & 7] + 1.0;
+  double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int j = 0; j < 4; ++j) s += c[j][0] + c[j][1];
+  if (s == 12345.678) out[11] = s;
+}
+
+int dmma_main() {
+  double* d;
+  cudaMalloc(&d, 1 << 20);
+  cudaMemset(d, 0, 1 << 20);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int m = 1 << 12;
+  for (int warps = 4; warps <= 16; warps *= 2) {
+    for (int pass = 0; pass < 2; ++pass) {
+      cudaEventRecord(a);
+      dmma_tp<<<sms * 2, 32 * warps>>>(d, m);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (pass)
+        printf("DMMA m8n8k4 (%d warps/CTA, 2 CTA/SM): %.1f TFLOP/s\n", warps,
+               2.0 * 256 * 4 * m * sms * 2 * warps / (ms * 1e9));
+    }
   }
   return 0;
 }
