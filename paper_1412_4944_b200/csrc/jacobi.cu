@@ -237,7 +237,7 @@ constexpr int kNsMaxIter = 48;
 // ---------------------------------------------------------------------------
 // Polar factor of a 64 x 64 P by the scaled Newton-Schulz iteration
 //   X_0 = P / ||P||_F,  X_{k+1} = X_k (1.5 a_k I - 0.5 a_k^3 X_k^T X_k),
-// a_k = sqrt(3 / (1 + l_k + l_k^2)), l_{k+1} = a_k l_k (3 - a_k^2 l_k^2) / 2, l_0 = 1e-8
+// a_k = sqrt(3 / (1 + l_k + l_k^2)), l_{k+1} = a_k l_k (3 - a_k^2 l_k^2) / 2, l_0 = 1e-6
 // (Chen & Chow scaling for singular values in [l_k, 1]).  Every iteration is two
 // dense 64^3 float64 GEMMs in shared memory — no sequential sweep steps — and it
 // converges to the same orthogonal factor U V^T the SVD gives (~1e-12 at
@@ -281,7 +281,9 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
   const double inv = 1.0 / nrm;
   for (int e = tid; e < N * N; e += kJacobiThreads) X[(e >> 6) * LD + (e & 63)] *= inv;
   __syncthreads();
-  double l = 1e-8;
+  // lower bound for sigma_min / ||P||_F (image-patch P: ~7e-6); an overestimate only
+  // slows the smallest singular values to plain Newton-Schulz speed
+  double l = 1e-6;
   int it = 0;
   bool done = false;
   const int row = 8 * warp + g;  // this thread's output row in both GEMMs

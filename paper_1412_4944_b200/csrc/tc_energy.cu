@@ -65,9 +65,12 @@ struct Ring {
 // split representation 3 * 2^-22 and fp32 accumulation of 192 exact products
 __device__ __forceinline__ float coef_err(float s_norm) { return 2.5e-6f * sqrtf(s_norm); }
 
-// bound on |R_hat - R| for a block with n discarded coefficients
+// bound on |R_hat - R| for a block with n discarded coefficients: coefficient
+// errors (Cauchy-Schwarz over the discarded set, which may differ from the exact
+// one only among near-equal magnitudes) plus the fp32 sum of <= 64 small terms
 __device__ __forceinline__ float resid_err(float r, float s, float d, int n) {
-  return 2.0f * d * sqrtf(static_cast<float>(n) * fmaxf(r, 0.0f)) + n * d * d + 1.2e-6f * s;
+  (void)s;
+  return 2.0f * d * sqrtf(static_cast<float>(n) * fmaxf(r, 0.0f)) + n * d * d + 8e-6f * fmaxf(r, 0.0f);
 }
 
 template <int G, bool ABS>
@@ -191,13 +194,19 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           float sq = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
 #pragma unroll
           for (int i = 0; i < 64; ++i) v[i] = ABS ? fabsf(v[i]) : v[i] * v[i];
-          topk::top_of_64<G>(v);
+          // squared-sum: the discarded energy R is summed from the values the
+          // network drops (+ the tail of the top-G list beyond k): no S - kept cancellation
+          float dropped = 0.0f;
+          if constexpr (ABS) topk::top_of_64<G>(v);
+          else dropped = topk::top_of_64_dropped<G>(v);
           float kept = 0.0f, e = 0.0f;
 #pragma unroll
           for (int i = 0; i < G; ++i) {
             if (i < ksel) {
               kept += ABS ? v[i] * v[i] : v[i];
               e += v[i];
+            } else if (!ABS) {
+              dropped += v[i];
             }
           }
           // unscale by 2^-(e_s + f_b), exact
@@ -206,7 +215,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           sq *= u2;
           kept *= u2;
           e *= ABS ? u : u2;
-          const float r = sq - kept;
+          const float r = ABS ? sq - kept : dropped * u2;
           const float dec = ABS ? -e : r;
           if (dec < d1) {
             d2 = d1;

@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
         const int64_t col = out_by_signal ? rows[s] : (t0 + s);
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          if ((r.mask >> u) & 1u) {
+          if (idx && ((r.mask >> u) & 1u)) {  // idx == NULL: residuals only
             const int i = qd + 4 * u;
             const int at = quad_position(masks, i);
             idx[at * ld + col] = static_cast<int16_t>(i);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
       for (int t = 0; t < T; ++t) {
         const bool on = (r.sel >> t) & 1u;
         const unsigned bal = __ballot_sync(0xffffffffu, on);
-        if (on) {
+        if (on && idx) {
           const int at = pos + __popc(bal & lt);
           idx[at * ld + col] = static_cast<int16_t>(lane + 32 * t);
           val[at * ld + col] = Cs[lane + 32 * t];

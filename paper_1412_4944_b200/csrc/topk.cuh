@@ -69,5 +69,31 @@ __device__ __forceinline__ void top_of_64(float* v) {
   }
 }
 
+// As top_of_64, also summing every value the network discards (each merge
+// keeps max(a_i, b_{G-1-i}) and drops the min): sum(v) = sum(top) + dropped,
+// with dropped accumulated from the small values themselves (no cancellation).
+template <int G>
+__device__ __forceinline__ float top_of_64_dropped(float* v) {
+  float dropped = 0.0f;
+#pragma unroll
+  for (int g = 0; g < 64; g += G) sort_desc<G>(v + g);
+#pragma unroll
+  for (int step = G; step < 64; step <<= 1) {
+#pragma unroll
+    for (int g = 0; g + step < 64; g += 2 * step) {
+      float* a = v + g;
+      const float* b = v + g + step;
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const float x = a[i], y = b[G - 1 - i];
+        a[i] = fmaxf(x, y);
+        dropped += fminf(x, y);
+      }
+      merge_desc<G>(a);
+    }
+  }
+  return dropped;
+}
+
 }  // namespace topk
 }  // namespace sbo

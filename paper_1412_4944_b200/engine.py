@@ -331,7 +331,7 @@ class Engine:
                    _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
                    g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, self.blocks.data_ptr(),
                    block_override, self.s0, self.kind, int(out_by_signal), ld,
-                   idx.data_ptr(), val.data_ptr(), _ptr(energy), _ptr(kept), self.stream,
+                   _ptr(idx), _ptr(val), _ptr(energy), _ptr(kept), self.stream,
                    units=self.m if order is not None and g.bounds is not None else 0)
 
     # ----------------------------------------------------------- training
@@ -410,9 +410,7 @@ class Engine:
             # float64 (exact support + discarded energy), as the worst set needs
             g = self.group(self.K)
             ld = max(self.m, 1)
-            idx = self.scratch.get("rep_idx", 2 * self.k * ld).view(torch.int16)
-            val = self.scratch.get("rep_val", 8 * self.k * ld).view(torch.float64)
-            self.code(g.perm, g, -1, True, ld, idx, val, None, self.state.residual)
+            self.code(g.perm, g, -1, True, ld, None, None, None, self.state.residual)
         self.residual()
 
     def rmse(self) -> float:
