@@ -1,0 +1,47 @@
+"""Summarize ncu --set full captures (.ncu-rep) into the metrics the DESIGN cites.
+
+    python tools/ncu_summary.py gpurun_out/full_*.ncu-rep > profiles/rNN_ncu_summary.txt
+"""
+import csv
+import io
+import subprocess
+import sys
+
+WANT = [
+    "gpu__time_duration.sum", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
+    "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "lts__t_bytes.sum", "smsp__inst_executed.sum",
+]
+
+
+def main():
+    for path in sys.argv[1:]:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        if len(rows) < 3:
+            print(f"== {path}: no data")
+            continue
+        hdr, unit = rows[0], rows[1]
+        for v in rows[2:]:
+            d = dict(zip(hdr, v))
+            print(f"== {path}  kernel={d.get('Kernel Name', '?')[:60]}")
+            for i, n in enumerate(hdr):
+                if n in WANT:
+                    print(f"  {n:78s} {v[i]:>16s} {unit[i]}")
+
+
+if __name__ == "__main__":
+    main()
