@@ -126,9 +126,10 @@ FP64_PEAK_TFLOPS = 33.0  # measured FFMA.F64 throughput on this pool (profiles/f
 
 
 def kernel_families(timer, p, k):
-    fam = {"sbo_round_segments": ("k_round_f64", 2 * p * p + 2 * p * k, "fp64 CUDA cores"),
+    fam = {"sbo_round_segments": ("k_round_f64", 2 * p * p + 2 * p * k, "fp64 tensor cores (DMMA)"),
            "sbo_tc_energy": ("k_energy_tc", 2 * p * p, "tcgen05 split-fp16"),
            "sbo_code_segments": ("k_code_f64", 2 * p * p, "fp64 CUDA cores"),
+           "sbo_residual_segments": ("k_round_f64<resid>", 2 * p * p, "fp64 tensor cores (DMMA)"),
            "sbo_polar": ("k_polar_ns", 0, "fp64 CUDA cores (latency)"),
            "sbo_energy_recheck": ("k_energy_f64 recheck", 0, "fp64 CUDA cores")}
     out = {}

@@ -155,6 +155,15 @@ int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
                        const int32_t* nseg, int64_t max_seg, const double* blocks,
                        int block_override, int s0, double* partial, void* stream);
 
+/* Squared residuals of represent (sbo.py:213-218) for p <= 64, min(s0, p) < 16:
+ * every signal of a segment is coded in its segment's block in float64 (exact
+ * selection, as sbo_code_segments) and rest_sq[order[t]] receives the energy of
+ * its discarded coefficients.  Replaces sbo_code_segments(idx = val = NULL). */
+int sbo_residual_segments(const void* y, int dtype, int p, const int32_t* order,
+                          const int32_t* seg_block, const int64_t* seg_lo, const int64_t* seg_hi,
+                          const int32_t* nseg, int64_t max_seg, const double* blocks, int s0,
+                          double* rest_sq, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Gram matrix G = Y_W Y_W^T of a member list (float64) — the data term of the
  * new block's initialisation (onb.py:79-95 via thin_svd(ysub), linalg.py:52).

@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace sbo {
 
@@ -352,6 +353,180 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
   if (tid == 0) status[b] = SBO_ST_OK | (it << 8) | (1 << 16);  // bit 16: Newton-Schulz
 }
 
+// ---------------------------------------------------------------------------
+// The same scaled Newton-Schulz iteration spread over a cluster of 4 CTAs per
+// matrix (one per SM), exchanging through distributed shared memory.  CTA r
+// owns the column slice J_r = [16r, 16r+16):
+//   G rows J_r    = X[:, J_r]^T X                         (local, full X held)
+//   A cols J_r    = c1 I + c3 G[J_r, :]^T                 (G symmetric: local)
+//   X' cols J_r   = X A[:, J_r]                           (local)
+// and pushes its X' slice into every CTA's next-X buffer with one bulk copy per
+// peer, completing transaction bytes on the receiver's mbarrier: one all-gather per
+// iteration, no cluster barrier (a receiver's "full" wait of iteration k also
+// proves every peer has finished reading the buffer it will overwrite in k+1,
+// since peers push only after their last read of it).  The convergence test of
+// X_k (the deviation ||X_k^T X_k - I||_F, a sum of per-CTA partials pushed with
+// the slice) is read after the wait; X_{k+1} is computed speculatively
+// meanwhile, so a converged X_k is still in the other buffer.  All CTAs take identical decisions
+// (same partial sums in the same order), so the cluster leaves the loop together.
+// ---------------------------------------------------------------------------
+constexpr int kNsCluster = 4;
+
+// DSMEM helpers: shared::cluster addresses and cluster-scope release/acquire
+// (generic stores would make the barrier fence at GPU scope)
+__device__ __forceinline__ uint32_t cluster_addr(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(local))), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// X is held slice-major: Xs[q][k][c] = X[k][16q + c] with a 20-double row stride
+// (conflict-free DMMA fragments), so a CTA's slice is one contiguous 10-KB block
+// that a single cp.async.bulk shared::cta -> shared::cluster copy delivers to a
+// peer (completing on the peer's mbarrier).  The slice's padding column 16 of
+// row 0 carries the CTA's deviation partial.
+constexpr int kNsSliceLd = 20;
+constexpr int kNsSlice = 64 * kNsSliceLd;  // doubles per slice
+
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, uint32_t bytes,
+                                               uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThreads)
+    k_polar_ns_cluster(const double* __restrict__ P, const int64_t* __restrict__ counts,
+                       double* Q, int32_t* status) {
+  constexpr int N = 64, NC = kNsCluster, W = N / NC, SL = kNsSliceLd, SZ = kNsSlice;
+  static_assert(W == 16, "the fragment mapping below assumes 16-column slices");
+  const int r = static_cast<int>(blockIdx.x % NC);  // == %cluster_ctarank for 1-D clusters
+  const int b = blockIdx.x / NC;
+  __shared__ double red[32];
+  __shared__ __align__(8) uint64_t full[2];
+  extern __shared__ __align__(128) unsigned char dyn[];
+  double* X0 = reinterpret_cast<double*>(dyn);  // buffer u, slice q: X0 + (u * NC + q) * SZ
+  constexpr int AL = kNsSliceLd;
+  double* As = X0 + 2 * NC * SZ;                // A[:, J_r] as As[j][i] (stride AL)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  if (counts && counts[b] == 0) {
+    if (tid == 0 && r == 0) status[b] = SBO_ST_SKIPPED;
+    return;
+  }
+  auto at = [&](int u, int k, int c) -> double* {  // &X_u[k][c]
+    return X0 + (u * NC + c / W) * SZ + k * SL + (c % W);
+  };
+  const double* Pb = P + static_cast<int64_t>(b) * N * N;
+  double nrm = 0.0;
+  for (int e = tid; e < N * N; e += kJacobiThreads) {
+    const double v = Pb[e];
+    *at(0, e >> 6, e & 63) = v;
+    nrm = fma(v, v, nrm);
+  }
+  nrm = sqrt(block_sum<kJacobiThreads>(nrm, red));
+  if (!(nrm > 0.0)) {
+    if (tid == 0 && r == 0) status[b] = kStNsFallback;
+    return;
+  }
+  const double inv = 1.0 / nrm;
+  for (int e = tid; e < N * N; e += kJacobiThreads) *at(0, e >> 6, e & 63) *= inv;
+  if (tid == 0) {
+    sm100::mbar_init(&full[0], 1);
+    sm100::mbar_init(&full[1], 1);
+    sm100::fence_barrier_init();
+  }
+  // peers in the cluster must be running (barriers initialised) before their
+  // shared memory is written
+  cluster_barrier();
+  constexpr uint32_t kTx = (NC - 1) * SZ * sizeof(double);  // bytes received per iteration
+  uint32_t phases = 0u;  // bit u: parity of full[u]
+  double l = 1e-6;
+  int it = 0, cur = 0;
+  bool done = false;
+  for (; it < kNsMaxIter; ++it) {
+    const double* Xr = X0 + (cur * NC + r) * SZ;                    // this CTA's slice
+    const double* Xw = X0 + (cur * NC + warp / 2) * SZ + 8 * (warp & 1);  // columns 8 warp ..
+    // G[16r + 8a + g][8 warp + 2 t4 + h] = sum_k X[k][16r + 8a + g] X[k][8 warp + 2 t4 + h]
+    double gg[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+    for (int k0 = 0; k0 < N; k0 += 4) {
+      const double bv = Xw[(k0 + t4) * SL + g];
+#pragma unroll
+      for (int a2 = 0; a2 < 2; ++a2) dmma64(gg[a2][0], gg[a2][1], Xr[(k0 + t4) * SL + 8 * a2 + g], bv);
+    }
+    const int gj = 8 * warp + 2 * t4;
+    double dsum = 0.0;
+    const double al = l < 0.99 ? sqrt(3.0 / (1.0 + l + l * l)) : 1.0;
+    const double c1 = 1.5 * al, c3 = -0.5 * al * al * al;
+#pragma unroll
+    for (int a2 = 0; a2 < 2; ++a2) {
+      const int gi = W * r + 8 * a2 + g;
+      const double d0 = gg[a2][0] - (gi == gj ? 1.0 : 0.0);
+      const double d1 = gg[a2][1] - (gi == gj + 1 ? 1.0 : 0.0);
+      dsum = fma(d0, d0, fma(d1, d1, dsum));
+      // A[j][16r + i] = c1 [j == 16r + i] + c3 G[16r + i][j]
+      As[gj * AL + 8 * a2 + g] = c3 * gg[a2][0] + (gi == gj ? c1 : 0.0);
+      As[(gj + 1) * AL + 8 * a2 + g] = c3 * gg[a2][1] + (gi == gj + 1 ? c1 : 0.0);
+    }
+    const double part = block_sum<kJacobiThreads>(dsum, red);  // (syncs: As complete)
+    l = fmin(1.0, al * l * (3.0 - al * al * l * l) * 0.5);
+    // X'[8 warp + g][16r + 8a + 2 t4 + h] = sum_j X[8 warp + g][j] A[j][16r + 8a + 2 t4 + h]
+    double yy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+    for (int k0 = 0; k0 < N; k0 += 4) {
+      const double av = *at(cur, 8 * warp + g, k0 + t4);
+#pragma unroll
+      for (int a2 = 0; a2 < 2; ++a2)
+        dmma64(yy[a2][0], yy[a2][1], av, As[(k0 + t4) * AL + 8 * a2 + g]);
+    }
+    const int nxt = cur ^ 1;
+    double* mine = X0 + (nxt * NC + r) * SZ;
+#pragma unroll
+    for (int a2 = 0; a2 < 2; ++a2)
+      *reinterpret_cast<double2*>(mine + (8 * warp + g) * SL + 8 * a2 + 2 * t4) =
+          make_double2(yy[a2][0], yy[a2][1]);
+    if (tid == 0) mine[W] = part;
+    // generic-proxy writes -> visible to the bulk-copy (async) proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      sm100::mbar_expect_tx(&full[nxt], kTx);
+#pragma unroll 1
+      for (int q = 1; q < NC; ++q) {
+        const uint32_t peer = static_cast<uint32_t>((r + q) % NC);
+        bulk_s2cluster(cluster_addr(mine, peer), mine, SZ * sizeof(double),
+                       cluster_addr(&full[nxt], peer));
+      }
+    }
+    sm100::mbar_wait(&full[nxt], (phases >> nxt) & 1u);
+    phases ^= 1u << nxt;
+    double dev = 0.0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) dev += X0[(nxt * NC + q) * SZ + W];
+    if (sqrt(dev) < 1e-13) {
+      done = true;
+      break;
+    }
+    cur = nxt;
+  }
+  if (!done) {
+    if (tid == 0 && r == 0) status[b] = kStNsFallback;
+    return;
+  }
+  double* Qb = Q + static_cast<int64_t>(b) * N * N;
+  for (int e = tid; e < W * N; e += kJacobiThreads) {
+    const int row = W * r + (e >> 6), col = e & 63;
+    Qb[row * N + col] = *at(cur, row, col);
+  }
+  if (tid == 0 && r == 0) status[b] = SBO_ST_OK | (it << 8) | (1 << 16);  // bit 16: Newton-Schulz
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restrict__ P, int p,
                                                           const int64_t* __restrict__ counts,
@@ -605,11 +780,23 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
   static const bool force_jacobi = getenv("SBO_POLAR_JACOBI") != nullptr;
   const bool ns = p == 64 && status && !sigma && !force_jacobi;
   if (ns) {
-    const size_t nsb = sizeof(double) * 3 * 64 * 68;
-    cudaFuncSetAttribute(k_polar_ns, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(nsb));
-    k_polar_ns<<<K, kJacobiThreads, nsb, as_stream(stream)>>>(P, counts, Q, status);
-    if (int rc = check_launch("k_polar_ns")) return rc;
+    static const bool single = getenv("SBO_POLAR_SINGLE_CTA") != nullptr;
+    if (single) {
+      const size_t nsb = sizeof(double) * 3 * 64 * 68;
+      cudaFuncSetAttribute(k_polar_ns, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(nsb));
+      k_polar_ns<<<K, kJacobiThreads, nsb, as_stream(stream)>>>(P, counts, Q, status);
+      if (int rc = check_launch("k_polar_ns")) return rc;
+    } else {
+      // > half of an SM's shared memory: one CTA per SM, so the 8 CTAs of a
+      // cluster run on 8 SMs (they would otherwise pack 3 to an SM)
+      const size_t nsb = 120 * 1024;
+      cudaFuncSetAttribute(k_polar_ns_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(nsb));
+      k_polar_ns_cluster<<<K * kNsCluster, kJacobiThreads, nsb, as_stream(stream)>>>(
+          P, counts, Q, status);
+      if (int rc = check_launch("k_polar_ns_cluster")) return rc;
+    }
   }
   if (smem) {
     cudaFuncSetAttribute(k_polar<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

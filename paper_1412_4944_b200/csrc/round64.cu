@@ -1,0 +1,318 @@
+// The 1ONB round for p <= 64, min(s0, p) < 16 (onb.py:170-171), fused per block
+// segment: float64 projection on the DMMA tensor cores, exact top-k selection
+// in registers, and the sparse outer product P += Y X^T in signal order.
+//
+// * Projection: warp w computes signals [8w, 8w+8) x 64 atoms of a 64-signal
+//   tile with mma.sync m8n8k4 f64; the accumulator fragment leaves each quad
+//   of lanes (t4 = lane & 3) holding one signal's 64 coefficients, 16 per lane
+//   (atoms 8n + 2 t4 + h).  Nothing is written back to shared memory.
+// * Selection (select_top, onb.py:58-76): fp32 magnitudes are a monotone
+//   rounding of the float64 ones, so when the k-th and (k+1)-th largest fp32
+//   magnitudes differ the kept set is exactly {i : fp32|c_i| >= t_k} — the
+//   float64 stable-argsort set.  A quad bitonic network finds t_k; a signal
+//   whose fp32 k-th/(k+1)-th magnitudes tie is re-decided by its warp with the
+//   exact rank rule (pick_row).
+// * Outer product (sparse_outer, onb.py:127-134): the kept values are written as
+//   a dense X tile (zeros elsewhere) and P += Y^T X runs on DMMA in signal order
+//   (deterministic partials, no atomics).  A sparse DFMA form (2 p k flop per
+//   signal) was measured 1.6x slower: its per-signal bookkeeping is instruction-
+//   bound, while the dense DMMA form issues 1 instruction per 512 flop.
+// * Residual mode (represent's residual, sbo.py:213-218): the same projection and
+//   selection, writing the energy of the discarded coefficients per signal.
+#include "common.cuh"
+#include "pick.cuh"
+#include "topk.cuh"
+
+namespace sbo {
+namespace r64 {
+
+constexpr int LD = 68;  // float64 row stride of the block / X tiles (conflict-free fragments)
+constexpr int KMAX = 16;
+
+// Signal tiles are staged in their storage type: float32 rows (stride 72 floats,
+// conflict-free DMMA fragment loads, double-buffered: the next tile's cp.async
+// copies fly during this tile) or float64 rows (stride 68, single buffer).
+template <typename TY>
+struct Stage {
+  static constexpr int NB = sizeof(TY) == 4 ? 2 : 1;
+  static constexpr int YLD = sizeof(TY) == 4 ? 72 : 68;
+};
+
+template <typename TY>
+struct Layout {
+  size_t y_off, q_off, x_off, rows_off, scr_off, flag_off, bytes;
+  __host__ __device__ Layout() {
+    y_off = 0;                                                        // sY[buf][s][kk]
+    q_off = y_off + sizeof(TY) * Stage<TY>::NB * kTile * Stage<TY>::YLD;
+    q_off = (q_off + 15) & ~size_t(15);                               // sQ[kk][i] float64
+    x_off = q_off + sizeof(double) * 64 * LD;                         // X[s][i]
+    rows_off = x_off + sizeof(double) * kTile * LD;                   // rows[buf][s]
+    scr_off = rows_off + sizeof(int64_t) * Stage<TY>::NB * kTile;     // per-warp fallback row
+    flag_off = scr_off + sizeof(double) * 8 * 64;
+    bytes = flag_off + 8 * 64;
+  }
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;"); }
+
+__device__ __forceinline__ int atom_of(int u, int t4) { return 8 * (u >> 1) + 2 * t4 + (u & 1); }
+
+template <typename TY, bool kResid>
+__global__ void __launch_bounds__(kThreads, 2) k_round64(
+    const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
+    const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
+    const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
+    const double* __restrict__ blocks, int block_override, int k, double* partial,
+    double* rest_sq) {
+  constexpr int NB = Stage<TY>::NB, YLD = Stage<TY>::YLD;
+  if (static_cast<int>(blockIdx.x) >= *nseg) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Layout<TY> L;
+  TY* sYall = reinterpret_cast<TY*>(smem + L.y_off);
+  double* sQ = reinterpret_cast<double*>(smem + L.q_off);
+  double* X = reinterpret_cast<double*>(smem + L.x_off);
+  int64_t* rowsall = reinterpret_cast<int64_t*>(smem + L.rows_off);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  double* scr = reinterpret_cast<double*>(smem + L.scr_off) + warp * 64;
+  unsigned char* fl = smem + L.flag_off + warp * 64;
+  const int seg = blockIdx.x;
+  const int b = block_override >= 0 ? block_override : seg_block[seg];
+  const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+  const double* q = blocks + static_cast<int64_t>(b) * p * p;
+  for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
+    const int kk = e >> 6, ii = e & 63;
+    sQ[kk * LD + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+  }
+  // P accumulator (outer mode), DMMA fragments: warp w owns rows [8w, 8w+8) x 64 atoms
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+
+  // stage tile [base, base + 64) into buffer `buf`; rows beyond hi / coordinates
+  // beyond p are zero.  p = 64: 16-B cp.async copies of whole rows (async);
+  // otherwise element loads (synchronous).
+  auto stage = [&](int64_t base, int buf) {
+    TY* sY = sYall + buf * kTile * YLD;
+    int64_t* rows = rowsall + buf * kTile;
+    if (tid < kTile) {
+      const int64_t t = base + tid;
+      rows[tid] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+    }
+    constexpr int CH = 64 * static_cast<int>(sizeof(TY)) / 16;  // 16-B chunks per row
+    if (p == 64) {
+      for (int e = tid; e < kTile * CH; e += kThreads) {
+        const int sl = e / CH, c = e % CH;
+        const int64_t t = base + sl;
+        const int64_t r = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+        cp_async16(sY + sl * YLD + c * (16 / sizeof(TY)), r >= 0 ? y + r * 64 + c * (16 / sizeof(TY)) : y,
+                   r >= 0);
+      }
+      cp_async_commit();
+    } else {
+      for (int e = tid; e < kTile * 64; e += kThreads) {
+        const int sl = e >> 6, kk = e & 63;
+        const int64_t t = base + sl;
+        const int64_t r = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
+        sY[sl * YLD + kk] = (r >= 0 && kk < p) ? __ldg(y + r * p + kk) : TY(0);
+      }
+    }
+  };
+  if (NB == 2) stage(lo, 0);
+  int it = 0;
+  for (int64_t t0 = lo; t0 < hi; t0 += kTile, ++it) {
+    const int buf = NB == 2 ? (it & 1) : 0;
+    if (NB == 1) {
+      __syncthreads();  // the previous tile is done with the buffer
+      stage(t0, 0);
+    }
+    cp_async_wait_all();
+    __syncthreads();  // tile `buf` landed everywhere; the previous tile is done with X / buf^1
+    if (NB == 2 && t0 + kTile < hi) stage(t0 + kTile, buf ^ 1);  // in flight during this tile
+    const TY* sY = sYall + buf * kTile * YLD;
+    const int64_t* rows = rowsall + buf * kTile;
+    // C = Y_tile . Q: this quad's signal s = 8 warp + g, coefficients c[n][h] of
+    // atoms 8n + 2 t4 + h
+    const int s = 8 * warp + g;
+    double c[8][2];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
+    {
+      const TY* ya = sY + s * YLD + t4;
+#pragma unroll 4
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const double a = static_cast<double>(ya[k0]);
+        const double* qb = sQ + (k0 + t4) * LD + g;
+#pragma unroll
+        for (int n = 0; n < 8; ++n) dmma(c[n][0], c[n][1], a, qb[8 * n]);
+      }
+    }
+    // exact selection in registers
+    const bool act = rows[s] >= 0;
+    // magnitudes are recomputed from c where needed (register pressure)
+    auto mag = [&](int u) -> float {
+      return (act && atom_of(u, t4) < p) ? static_cast<float>(fabs(c[u >> 1][u & 1])) : -1.0f;
+    };
+    float srt[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) srt[u] = mag(u);
+    topk::sort_desc<16>(srt);
+#pragma unroll
+    for (int x = 1; x <= 2; x <<= 1) {
+      float other[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) other[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
+      topk::merge_top<16>(srt, other);
+    }
+    float tk = srt[0], tk1 = srt[1];
+#pragma unroll
+    for (int u = 1; u < 16; ++u) {
+      if (u == k - 1) tk = srt[u];
+      if (u == k) tk1 = srt[u];
+    }
+    uint32_t mask = 0u;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (mag(u) >= tk && mag(u) >= 0.0f) mask |= 1u << u;
+    // float32 ties at the threshold: the warp re-decides those signals exactly
+    unsigned need = __ballot_sync(0xffffffffu, act && !(tk > tk1) && t4 == 0);
+    double rest = -1.0;  // < 0: not decided by the fallback
+    while (need) {
+      const int gg = (__ffs(need) - 1) >> 2;
+      need &= need - 1;
+      if (g == gg) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) scr[atom_of(u, t4)] = c[u >> 1][u & 1];
+      }
+      __syncwarp();
+      const RowPick r = pick_row(scr, p, k, SBO_KIND_SQUARED_SUM);
+      fl[lane] = r.sel & 1u;
+      fl[lane + 32] = (r.sel >> 1) & 1u;
+      __syncwarp();
+      if (g == gg) {
+        mask = 0u;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (fl[atom_of(u, t4)]) mask |= 1u << u;
+        rest = r.rest_sq;
+      }
+      __syncwarp();
+    }
+    if constexpr (kResid) {
+      // every lane takes part in the quad sum (full-mask shuffles), the
+      // fallback's exact value wins where it was computed
+      double d = 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const double v = c[u >> 1][u & 1];
+        if (!((mask >> u) & 1u) && mag(u) >= 0.0f) d = fma(v, v, d);
+      }
+      d += __shfl_xor_sync(0xffffffffu, d, 1);
+      d += __shfl_xor_sync(0xffffffffu, d, 2);
+      if (rest < 0.0) rest = d;
+      if (act && t4 == 0) rest_sq[rows[s]] = rest;
+    } else {
+      // X = the kept coefficients, zeros elsewhere (fragment layout -> rows of X)
+      double* xr = X + s * LD + 2 * t4;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+        *reinterpret_cast<double2*>(xr + 8 * n) =
+            make_double2(((mask >> (2 * n)) & 1u) ? c[n][0] : 0.0,
+                         ((mask >> (2 * n + 1)) & 1u) ? c[n][1] : 0.0);
+      __syncthreads();
+      // P[kk][i] += sum_s Y[s][kk] X[s][i] on DMMA, signals in order (inactive
+      // rows are zero in both Y and X)
+      const TY* ya = sY + t4 * YLD + 8 * warp + g;
+      const double* xb = X + t4 * LD + g;
+#pragma unroll 4
+      for (int s4 = 0; s4 < kTile; s4 += 4) {
+        const double av = static_cast<double>(ya[s4 * YLD]);
+#pragma unroll
+        for (int n = 0; n < 8; ++n) dmma(acc[n][0], acc[n][1], av, xb[s4 * LD + 8 * n]);
+      }
+    }
+  }
+  if constexpr (!kResid) {
+    double* out = partial + static_cast<int64_t>(seg) * p * p;
+    const int row = 8 * warp + g;
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * n + 2 * t4 + h;
+        if (row < p && col < p) out[row * p + col] = acc[n][h];
+      }
+  }
+}
+
+template <typename TY, bool kResid>
+int launch(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
+           const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+           const double* blocks, int block_override, int k, double* partial, double* rest_sq,
+           cudaStream_t st) {
+  const Layout<TY> L;
+  cudaFuncSetAttribute(k_round64<TY, kResid>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(L.bytes));
+  k_round64<TY, kResid><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
+      static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
+      block_override, k, partial, rest_sq);
+  return check_launch(kResid ? "k_round64<resid>" : "k_round64");
+}
+
+int check(int dtype, int p, int s0) {
+  if (dtype != SBO_F32 && dtype != SBO_F64) return fail(SBO_EINVAL, "bad dtype");
+  if (p < 1 || p > 64) return fail(SBO_EINVAL, "the fused round needs p <= 64");
+  const int k = s0 < p ? s0 : p;
+  if (s0 < 1 || k >= KMAX) return fail(SBO_EINVAL, "the fused round needs 1 <= min(s0, p) < 16");
+  return SBO_OK;
+}
+
+}  // namespace r64
+}  // namespace sbo
+
+using namespace sbo;
+
+extern "C" int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
+                                  const int32_t* seg_block, const int64_t* seg_lo,
+                                  const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                                  const double* blocks, int block_override, int s0,
+                                  double* partial, void* stream) {
+  if (int rc = r64::check(dtype, p, s0)) return rc;
+  if (max_seg <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? r64::launch<float, false>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+                                         blocks, block_override, k, partial, nullptr,
+                                         as_stream(stream))
+             : r64::launch<double, false>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+                                          blocks, block_override, k, partial, nullptr,
+                                          as_stream(stream));
+}
+
+extern "C" int sbo_residual_segments(const void* y, int dtype, int p, const int32_t* order,
+                                     const int32_t* seg_block, const int64_t* seg_lo,
+                                     const int64_t* seg_hi, const int32_t* nseg,
+                                     int64_t max_seg, const double* blocks, int s0,
+                                     double* rest_sq, void* stream) {
+  if (int rc = r64::check(dtype, p, s0)) return rc;
+  if (!rest_sq) return fail(SBO_EINVAL, "rest_sq is required");
+  if (max_seg <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? r64::launch<float, true>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+                                        blocks, -1, k, nullptr, rest_sq, as_stream(stream))
+             : r64::launch<double, true>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+                                         blocks, -1, k, nullptr, rest_sq, as_stream(stream));
+}

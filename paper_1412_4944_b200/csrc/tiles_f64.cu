@@ -12,6 +12,7 @@
 // coefficient i is kept iff fewer than k coefficients beat it under the key
 // (|c| descending, index ascending) — the stable-argsort rule of onb.py:73.
 #include "common.cuh"
+#include "pick.cuh"
 #include "topk.cuh"
 
 namespace sbo {
@@ -125,60 +126,6 @@ __device__ void project_tile(const TY* __restrict__ y, int p, const int64_t* row
         if (4 * tx + b < in) C[(4 * ty + a) * ldc + ic + 4 * tx + b] = acc[a][b];
   }
   __syncthreads();
-}
-
-// Exact top-k of one coefficient row, warp-cooperative.  Lane l owns the
-// coefficients i = l + 32 t.  Returns the selected mask bit t in `sel`.
-struct RowPick {
-  unsigned sel;     // bit t: coefficient lane+32t kept
-  double score;     // warp-reduced: sum of kept c^2 (kind 0) or |c| (kind 1)
-  double rest_sq;   // warp-reduced: sum of the DISCARDED c^2 = ||y - Q x||^2
-};
-
-__device__ RowPick pick_row(const double* Cs, int p, int k, int kind) {
-  const int lane = threadIdx.x & 31;
-  const int T = (p + 31) >> 5;
-  double a[8];
-  int rank[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int i = lane + 32 * t;
-    a[t] = (t < T && i < p) ? fabs(Cs[i]) : -1.0;
-    rank[t] = 0;
-  }
-  for (int j = 0; j < p; ++j) {
-    const double cj = fabs(Cs[j]);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      if (t < T) {
-        const int i = lane + 32 * t;
-        rank[t] += (cj > a[t]) || (cj == a[t] && j < i);
-      }
-    }
-  }
-  RowPick r;
-  r.sel = 0u;
-  // The squared residual is accumulated from the discarded coefficients: equal
-  // to ||y||^2 - sum(kept^2) by Parseval (the reference's formula, sbo.py:218)
-  // but without its cancellation when the kept energy is close to ||y||^2.
-  double sc = 0.0, sq = 0.0, rest = 0.0;
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int i = lane + 32 * t;
-    if (t < T && i < p) {
-      const double c = Cs[i];
-      if (rank[t] < k) {
-        r.sel |= 1u << t;
-        sq = fma(c, c, sq);
-        sc += fabs(c);
-      } else {
-        rest = fma(c, c, rest);
-      }
-    }
-  }
-  r.score = warp_sum(kind == SBO_KIND_SQUARED_SUM ? sq : sc);
-  r.rest_sq = warp_sum(rest);
-  return r;
 }
 
 // Fast exact selection for p <= 64, k <= 15: four lanes per signal (a quad);
@@ -578,8 +525,17 @@ __global__ void k_reduce_segments(const double* __restrict__ partial,
     s1 = 0;
   }
   if (e >= pp) return;
+  // loads batched 8 deep (independent), summed strictly in segment order
   double acc = 0.0;
-  for (int s = s0; s < s1; ++s) acc += partial[s * pp + e];
+  int s = s0;
+  for (; s + 8 <= s1; s += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(partial + (s + u) * pp + e);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
+  for (; s < s1; ++s) acc += __ldcs(partial + s * pp + e);
   P[b * pp + e] = acc;
 }
 
@@ -593,220 +549,10 @@ __global__ void k_chunk_segments(int64_t w, int chunk, int64_t* lo, int64_t* hi,
   if (threadIdx.x == 0) *nseg = static_cast<int32_t>(n);
 }
 
-// ---------------------------------------------------------------------------
-// Fused 1ONB round for p <= 64, k < 16 (onb.py:170-171): per block segment,
-// code every signal in its block (float64 projection + exact quad selection)
-// and accumulate P = Y X^T, without writing the codes.  The block is staged in
-// shared memory once per segment; the masked coefficient tile is X in place.
-// ---------------------------------------------------------------------------
-// float64 row stride of the y / block / coefficient tiles: 68 doubles keeps the
-// DMMA fragment loads (4 rows x 4-8 consecutive doubles per half-warp) free of
-// shared-memory bank conflicts and rows 16-byte aligned
-constexpr int kRoundLd = 68;
-
-// D(8x8) += A(8x4) B(4x8) on the float64 tensor cores (mma.sync m8n8k4, DMMA).
-// Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
-// d0/d1 = D[lane>>2][2(lane&3)], D[lane>>2][2(lane&3)+1].
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-struct RoundLayout {
-  size_t y_off, q_off, c_off, rows_off, fb_off, bytes;
-  __host__ __device__ RoundLayout() {
-    y_off = 0;                                          // sY[s][kk]
-    q_off = y_off + sizeof(double) * 64 * kRoundLd;      // sQ[kk][i]
-    c_off = q_off + sizeof(double) * 64 * kRoundLd;      // C[s][i] -> X[s][i]
-    rows_off = c_off + sizeof(double) * kTile * kRoundLd;
-    fb_off = rows_off + sizeof(int64_t) * kTile;
-    bytes = fb_off + sizeof(int) * kTile;
-  }
-};
-
-template <typename TY>
-__global__ void __launch_bounds__(kThreads, 2) k_round_f64(
-    const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
-    const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
-    const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
-    const double* __restrict__ blocks, int block_override, int k, double* partial) {
-  if (static_cast<int>(blockIdx.x) >= *nseg) return;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const RoundLayout L;
-  double* sY = reinterpret_cast<double*>(smem + L.y_off);
-  double* sQ = reinterpret_cast<double*>(smem + L.q_off);
-  double* C = reinterpret_cast<double*>(smem + L.c_off);
-  int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
-  int* fb = reinterpret_cast<int*>(smem + L.fb_off);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int seg = blockIdx.x;
-  const int b = block_override >= 0 ? block_override : seg_block[seg];
-  const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
-  const double* q = blocks + static_cast<int64_t>(b) * p * p;
-  for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
-    const int kk = e >> 6, ii = e & 63;
-    sQ[kk * kRoundLd + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
-  }
-  // P accumulator: warp w owns rows [8w, 8w+8) x 64 atoms as 8 DMMA tiles
-  const int g = lane >> 2, t4 = lane & 3;
-  double acc[8][2];
-#pragma unroll
-  for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
-
-  // Signal tiles are staged signal-major (sY[s][k]): coalesced global loads,
-  // contiguous stores, 16-byte reads in the outer product.  The next tile's
-  // values are prefetched into registers while the current tile computes.
-  // Thread t fetches signals (t >> 4) + 16 j, coordinates 4 (t & 15) .. + 3.
-  const int c4 = tid & 15;
-  TY pre[16];
-  int64_t prow[4];
-  auto fetch = [&](int64_t base) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t t = base + (tid >> 4) + 16 * j;
-      prow[j] = t < hi ? (order ? static_cast<int64_t>(order[t]) : t) : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t r = prow[j];
-      if (p == 64 && r >= 0) {
-        if constexpr (sizeof(TY) == 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(y + r * 64) + c4);
-          pre[4 * j] = v.x;
-          pre[4 * j + 1] = v.y;
-          pre[4 * j + 2] = v.z;
-          pre[4 * j + 3] = v.w;
-        } else {
-          const double2 v0 = __ldg(reinterpret_cast<const double2*>(y + r * 64) + 2 * c4);
-          const double2 v1 = __ldg(reinterpret_cast<const double2*>(y + r * 64) + 2 * c4 + 1);
-          pre[4 * j] = v0.x;
-          pre[4 * j + 1] = v0.y;
-          pre[4 * j + 2] = v1.x;
-          pre[4 * j + 3] = v1.y;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int kk = 4 * c4 + i;
-          pre[4 * j + i] = (r >= 0 && kk < p) ? __ldg(y + r * p + kk) : TY(0);
-        }
-      }
-    }
-  };
-  fetch(lo);
-  for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
-    __syncthreads();  // the previous tile's outer product is done with sY / C
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int s = (tid >> 4) + 16 * j;
-      *reinterpret_cast<double4*>(sY + s * kRoundLd + 4 * c4) =
-          make_double4(static_cast<double>(pre[4 * j]), static_cast<double>(pre[4 * j + 1]),
-                       static_cast<double>(pre[4 * j + 2]), static_cast<double>(pre[4 * j + 3]));
-      if (c4 == 0) rows[s] = prow[j];
-    }
-    __syncthreads();
-    if (t0 + kTile < hi) fetch(t0 + kTile);  // loads in flight during this tile
-    // C = Y_tile . Q on DMMA: warp w computes signals [8w, 8w+8) x 64 atoms
-    {
-      double c[8][2];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
-      const double* ya = sY + (8 * warp + g) * kRoundLd + t4;
-#pragma unroll 4
-      for (int k0 = 0; k0 < 64; k0 += 4) {
-        const double a = ya[k0];
-        const double* qb = sQ + (k0 + t4) * kRoundLd + g;
-#pragma unroll
-        for (int n = 0; n < 8; ++n) dmma(c[n][0], c[n][1], a, qb[8 * n]);
-      }
-      double* crow = C + (8 * warp + g) * kRoundLd + 2 * t4;
-#pragma unroll
-      for (int n = 0; n < 8; ++n)
-        *reinterpret_cast<double2*>(crow + 8 * n) = make_double2(c[n][0], c[n][1]);
-    }
-    __syncthreads();
-    // exact selection; non-kept coefficients are zeroed, so C becomes X
-    {
-      const int s = tid >> 2, qd = tid & 3;
-      const bool act = rows[s] >= 0;
-      double* Cs = C + s * kRoundLd;
-      const QuadPick r = quad_pick(Cs, p, k, SBO_KIND_SQUARED_SUM, act);
-      if (qd == 0) fb[s] = act && !r.ok;
-      if (r.ok) {
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (!((r.mask >> u) & 1u)) Cs[qd + 4 * u] = 0.0;
-      }
-    }
-    __syncthreads();
-    for (int s = warp; s < kTile; s += kThreads / 32) {
-      if (!fb[s]) continue;  // float32 tie: exact rank selection for this signal
-      double* Cs = C + s * kRoundLd;
-      const RowPick r = pick_row(Cs, p, k, SBO_KIND_SQUARED_SUM);
-      __syncwarp();
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-        if (!((r.sel >> t) & 1u)) Cs[lane + 32 * t] = 0.0;
-    }
-    __syncthreads();
-    // P[k][i] += sum_s Y[s][k] X[s][i] on DMMA: A = Y^T, B = X, signals in order
-    // (rows beyond the tile's signals are zero in both Y and X)
-    const double* ya = sY + t4 * kRoundLd + 8 * warp + g;
-    const double* xb = C + t4 * kRoundLd + g;
-#pragma unroll 4
-    for (int s0 = 0; s0 < kTile; s0 += 4) {
-      const double a = ya[s0 * kRoundLd];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) dmma(acc[n][0], acc[n][1], a, xb[s0 * kRoundLd + 8 * n]);
-    }
-  }
-  double* out = partial + static_cast<int64_t>(seg) * p * p;
-  const int row = 8 * warp + g;
-#pragma unroll
-  for (int n = 0; n < 8; ++n)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int col = 8 * n + 2 * t4 + h;
-      if (row < p && col < p) out[row * p + col] = acc[n][h];
-    }
-}
-
 }  // namespace sbo
 
 using namespace sbo;
 
-template <typename TY>
-static int round_impl(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
-                      const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
-                      int64_t max_seg, const double* blocks, int block_override, int k,
-                      double* partial, cudaStream_t st) {
-  const RoundLayout L;
-  cudaFuncSetAttribute(k_round_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(L.bytes));
-  k_round_f64<TY><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
-      static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
-      block_override, k, partial);
-  return check_launch("k_round_f64");
-}
-
-extern "C" int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
-                                  const int32_t* seg_block, const int64_t* seg_lo,
-                                  const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
-                                  const double* blocks, int block_override, int s0,
-                                  double* partial, void* stream) {
-  if (dtype != SBO_F32 && dtype != SBO_F64) return fail(SBO_EINVAL, "bad dtype");
-  if (p < 1 || p > 64) return fail(SBO_EINVAL, "the fused round needs p <= 64");
-  const int k = s0 < p ? s0 : p;
-  if (s0 < 1 || k >= 16) return fail(SBO_EINVAL, "the fused round needs 1 <= min(s0, p) < 16");
-  if (max_seg <= 0) return SBO_OK;
-  return dtype == SBO_F32
-             ? round_impl<float>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
-                                 block_override, k, partial, as_stream(stream))
-             : round_impl<double>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg, blocks,
-                                  block_override, k, partial, as_stream(stream));
-}
 
 namespace {
 template <typename TY>

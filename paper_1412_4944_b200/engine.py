@@ -409,8 +409,15 @@ class Engine:
             # float32-accurate, so recode every signal in its winning block in
             # float64 (exact support + discarded energy), as the worst set needs
             g = self.group(self.K)
-            ld = max(self.m, 1)
-            self.code(g.perm, g, -1, True, ld, None, None, None, self.state.residual)
+            if self.p <= 64 and self.k < 16:
+                self._call("sbo_residual_segments", self.sig.y.data_ptr(), self.sig.code,
+                           self.p, g.perm.data_ptr(), g.seg_block.data_ptr(),
+                           g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(),
+                           g.max_seg, self.blocks.data_ptr(), self.s0,
+                           self.state.residual.data_ptr(), self.stream, units=self.m)
+            else:
+                ld = max(self.m, 1)
+                self.code(g.perm, g, -1, True, ld, None, None, None, self.state.residual)
         self.residual()
 
     def rmse(self) -> float:

@@ -375,3 +375,32 @@ def test_sbo_train_fixed_point():
     d, code, a, rep = S.sbo_train(q_star @ x, S.SboConfig(s0=1, k0=1, p0=40, k_max=8,
                                                          target_error=1e-8, seed=5, rounds=4))
     assert d.num_blocks == 1 and rep.rows[-1].rmse <= 1e-8
+
+
+def test_iteration_zero_and_duplicate_signals(dev):
+    """Multi-tile segments mixing all-zero signals (every coefficient ties at 0: the
+    exact rank fallback, index order), small duplicated signals (scaled below the
+    worst set, which would otherwise be rank-deficient) and Gaussian ones:
+    represent, the fused rounds and the residual pass vs the oracle."""
+    rng = np.random.default_rng(21)
+    p, m, K, s0 = 64, 24576, 4, 8
+    y32 = rng.standard_normal((m, p)).astype(np.float32)
+    y32[rng.random(m) < 0.2] = 0.0
+    dup = rng.random(m) < 0.2
+    y32[dup] = 0.05 * y32[np.flatnonzero(~dup)[:7]][rng.integers(0, 7, dup.sum())]
+    blocks = [np.linalg.qr(rng.standard_normal((p, p)))[0] for _ in range(K)]
+    eng = _engine(dev, y32, blocks, s0)
+    y64 = y32.T.astype(np.float64)
+    rep0 = O.code_signals(y64, blocks, s0)
+    np.testing.assert_array_equal(eng.state.best.cpu().numpy(), rep0.block)
+    np.testing.assert_allclose(eng.state.residual.cpu().numpy(), rep0.residual_sq,
+                               rtol=1e-9, atol=1e-12)
+    draws = _block_rng(0, 1, K).standard_normal((p + 8, p))
+    out = eng.iterate(m // 16, 3, draws)
+    tr = O.iterate(y64, blocks, rep0.residual_sq, s0, 3, m // 16, seed=0)
+    np.testing.assert_array_equal(np.sort(out.worst.cpu().numpy()), np.sort(tr.worst))
+    got = eng.blocks[: eng.K].cpu().numpy()
+    assert max(np.abs(a - b).max() for a, b in zip(got, tr.blocks)) < 1e-9
+    np.testing.assert_array_equal(eng.state.best.cpu().numpy(), tr.rep2.block)
+    np.testing.assert_allclose(eng.state.residual.cpu().numpy(), tr.rep2.residual_sq,
+                               rtol=1e-9, atol=1e-12)
