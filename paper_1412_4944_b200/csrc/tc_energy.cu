@@ -166,10 +166,27 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
     const int row = 32 * q + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q) << 16);
     Ring racc;
+    // per-signal inputs of the NEXT tile are loaded while this tile computes
+    // (their global-memory latency would otherwise sit on every tile's path)
+    // (raw values: converting here would wait for the load)
+    auto preload = [&](int64_t tt, int& es_, double& prev_) {
+      const int64_t jj = tt * M + row;
+      es_ = 0;
+      prev_ = ABS ? -INFINITY : INFINITY;
+      if (tt < ntiles && jj < m) {
+        es_ = escale[jj];
+        if (accumulate) prev_ = ABS ? __ldcg(score + jj) : __ldcg(residual + jj);
+      }
+    };
+    int es_next;
+    double prev_next;
+    preload(blockIdx.x, es_next, prev_next);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t j = t * M + row;
       const bool valid = j < m;
-      const int es = valid ? escale[j] : 0;
+      const int es = es_next;
+      const double prev_pre = prev_next;
+      preload(t + gridDim.x, es_next, prev_next);
       float d1 = INFINITY, d2 = INFINITY, rb = 0.0f, eb = 0.0f, snorm = 0.0f;
       int bb = -1;
       for (int c = 0; c < nchunks; ++c) {
@@ -265,7 +282,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
         };
         bool flag;
         if (accumulate) {  // incoming winner covers blocks < b0 and keeps ties
-          const float prev = ABS ? -static_cast<float>(score[j]) : static_cast<float>(residual[j]);
+          const float prev = ABS ? -static_cast<float>(prev_pre) : static_cast<float>(prev_pre);
           flag = fabsf(d1 - prev) <= err(d1) + err(prev);
           if (d1 < prev) {
             best[j] = bb;

@@ -321,8 +321,10 @@ class Engine:
         nseg = max(1, math.ceil(n / sl)) if n > 0 else 0
         lo = torch.arange(0, max(n, 1), sl, dtype=torch.int64, device=self.dev)[:nseg]
         hi = torch.clamp(lo + sl, max=n)
+        # torch.full, not torch.tensor: no pageable host->device copy (which would
+        # synchronise the host with the queued kernels mid-iteration)
         return Groups(None, None, torch.zeros(max(nseg, 1), dtype=torch.int32, device=self.dev),
-                      lo, hi, torch.tensor([nseg], dtype=torch.int32, device=self.dev),
+                      lo, hi, torch.full((1,), nseg, dtype=torch.int32, device=self.dev),
                       max(nseg, 1))
 
     def code(self, order, g: Groups, block_override: int, out_by_signal: bool, ld: int,
@@ -382,7 +384,21 @@ class Engine:
 
     def init_block(self, G, ncols: int, draws: np.ndarray, slot: int, status, rank=None):
         self.reset_rotation(slot, slot + 1)
-        d = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).to(self.dev)
+        # staged through a persistent pinned buffer and copied asynchronously (a
+        # pageable copy would synchronise); the buffer is reused only after the
+        # iteration's closing synchronisation
+        host = np.ascontiguousarray(draws, dtype=np.float64)
+        pin = getattr(self, "_draws_pin", None)
+        done = getattr(self, "_draws_done", None)
+        if done is not None:
+            done.synchronize()  # the previous copy out of the buffer has run
+        if pin is None or pin.numel() < host.size:
+            pin = self._draws_pin = torch.empty(host.size, dtype=torch.float64).pin_memory()
+        pin[: host.size].copy_(torch.from_numpy(host.reshape(-1)))
+        d = torch.empty(host.shape, dtype=torch.float64, device=self.dev)
+        d.view(-1).copy_(pin[: host.size], non_blocking=True)
+        self._draws_done = torch.cuda.Event()
+        self._draws_done.record()
         ws = self.scratch.get("init", L.size("sbo_init_workspace_bytes", self.p))
         self._call("sbo_init_block", G.data_ptr(), self.p, ncols, d.data_ptr(), d.shape[0],
                    self.block_ptr(slot), _ptr(rank), status.data_ptr(), ws.data_ptr(),
