@@ -260,11 +260,11 @@ def run_ours(a):
     draws = _block_rng(1, 1, K0).standard_normal((p + 8, p))
     w = max(p, m_total // 16)
 
+    # the entering state of every step: blocks and assignment (Engine.snapshot)
+    entering = eng.snapshot()
+
     def restore():
-        eng.blocks.copy_(snap_blocks)
-        for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total), snap):
-            dst.copy_(src)
-        eng.K = K0
+        eng.restore(entering)
 
     class Marks:
         def __init__(self):
@@ -396,6 +396,7 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
 
     def step():
         eng.sig.y.copy_(host_y, non_blocking=True)
+        eng.refresh_signals()  # device-side operand split of the uploaded signals
         eng.blocks[:K0].copy_(host_blocks, non_blocking=True)
         for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total),
                             host_state):

@@ -200,6 +200,11 @@ class Engine:
             self.flags = torch.empty(self.m, dtype=torch.int32, device=self.dev)
             self.nflag = torch.zeros(1, dtype=torch.int32, device=self.dev)
             self._alloc_tc_blocks(self.k_cap)
+            self.refresh_signals()
+
+    def refresh_signals(self):
+        """Re-derive the tensor-core operands (split fp16) after the signals changed."""
+        if self.tc:
             self._call("sbo_tc_split_signals", self.sig.y.data_ptr(), self.sig.code, self.m,
                        self.p, self.yh.data_ptr(), self.yl.data_ptr(), self.escale.data_ptr(),
                        self.stream)
@@ -239,6 +244,20 @@ class Engine:
         self.blocks[:K].copy_(t.to(self.dev))
         self.reset_rotation(0, K)
         self.K = K
+
+    def snapshot(self) -> dict:
+        """Device copy of the iteration-entering state (blocks, assignment)."""
+        st = self.state
+        return {"K": self.K, "blocks": self.blocks.clone(),
+                "state": [t.clone() for t in (st.best, st.score, st.norm, st.residual, st.total)]}
+
+    def restore(self, snap: dict):
+        """Return to a snapshot's state (device-to-device copies, stream-ordered)."""
+        st = self.state
+        self.blocks.copy_(snap["blocks"])
+        for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total), snap["state"]):
+            dst.copy_(src)
+        self.K = snap["K"]
 
     def reset_rotation(self, b0: int, b1: int):
         """Identity warm start for the polar Jacobi of blocks [b0, b1)."""
