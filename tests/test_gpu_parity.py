@@ -404,3 +404,28 @@ def test_iteration_zero_and_duplicate_signals(dev):
     np.testing.assert_array_equal(eng.state.best.cpu().numpy(), tr.rep2.block)
     np.testing.assert_allclose(eng.state.residual.cpu().numpy(), tr.rep2.residual_sq,
                                rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("p,K,s0,m", [(64, 3, 16, 6000), (64, 3, 32, 4000), (16, 4, 4, 5000),
+                                      (256, 2, 16, 32768)])
+def test_iteration_other_shapes_against_oracle(dev, p, K, s0, m):
+    """Configs D/E shapes (p = 256, s0 in {16, 32}) and a small p: the general float64
+    path (no fused round) through one full teacher-free iteration vs the oracle."""
+    rng = np.random.default_rng(1000 * p + s0)
+    y32 = rng.standard_normal((m, p)).astype(np.float32)
+    blocks = [np.linalg.qr(rng.standard_normal((p, p)))[0] for _ in range(K)]
+    eng = _engine(dev, y32, blocks, s0)
+    y64 = y32.T.astype(np.float64)
+    rep0 = O.code_signals(y64, blocks, s0)
+    np.testing.assert_array_equal(eng.state.best.cpu().numpy(), rep0.block)
+    w = max(p, m // 16)
+    draws = _block_rng(0, 1, K).standard_normal((p + 8, p))
+    out = eng.iterate(w, 2, draws)
+    tr = O.iterate(y64, blocks, rep0.residual_sq, s0, 2, w, seed=0)
+    np.testing.assert_array_equal(np.sort(out.worst.cpu().numpy()), np.sort(tr.worst))
+    got = eng.blocks[: eng.K].cpu().numpy()
+    assert max(np.abs(a - b).max() for a, b in zip(got, tr.blocks)) < 1e-8
+    np.testing.assert_array_equal(eng.state.best.cpu().numpy(), tr.rep2.block)
+    np.testing.assert_allclose(eng.state.residual.cpu().numpy(), tr.rep2.residual_sq,
+                               rtol=1e-9, atol=1e-12)
+    assert out.rmse == pytest.approx(tr.rmse, rel=1e-10)
