@@ -71,11 +71,14 @@ int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const double* bl
                     int b1, int s0, int kind, int accumulate, int32_t* best, double* score,
                     double* residual_sq, double* norm_sq, void* stream);
 
-/* Exact float64 re-decision of the signals list[0 .. *nlist) over all K blocks:
+/* Exact float64 re-decision of the signals list[0 .. *nlist) over blocks [b0, K):
  * rewrites their best / score / residual_sq (the certification step after the
- * tensor-core energy pass flags near-ties).  max_list bounds *nlist (grid size). */
-int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p, const double* blocks, int K,
-                       int s0, int kind, const int32_t* list, const int32_t* nlist,
+ * tensor-core energy pass flags near-ties).  b0 > 0 is the incremental form
+ * (represent after a block was appended, sbo.py:361): the incoming best / score /
+ * residual_sq stand for blocks < b0 and must be exact (sbo_residual_segments
+ * writes exact scores); ties keep the lower block.  max_list bounds *nlist. */
+int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p, const double* blocks, int b0,
+                       int K, int s0, int kind, const int32_t* list, const int32_t* nlist,
                        int64_t max_list, int32_t* best, double* score, double* residual_sq,
                        void* stream);
 
@@ -158,11 +161,12 @@ int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
 /* Squared residuals of represent (sbo.py:213-218) for p <= 64, min(s0, p) < 16:
  * every signal of a segment is coded in its segment's block in float64 (exact
  * selection, as sbo_code_segments) and rest_sq[order[t]] receives the energy of
- * its discarded coefficients.  Replaces sbo_code_segments(idx = val = NULL). */
+ * its discarded coefficients; score (optional) the exact energy of the kind
+ * (block_energy, sbo.py:126-135).  Replaces sbo_code_segments(idx = val = NULL). */
 int sbo_residual_segments(const void* y, int dtype, int p, const int32_t* order,
                           const int32_t* seg_block, const int64_t* seg_lo, const int64_t* seg_hi,
                           const int32_t* nseg, int64_t max_seg, const double* blocks, int s0,
-                          double* rest_sq, void* stream);
+                          int kind, double* rest_sq, double* score, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Gram matrix G = Y_W Y_W^T of a member list (float64) — the data term of the

@@ -25,7 +25,7 @@ _SIGS = {
     "sbo_last_error": (C.c_char_p, []),
     "sbo_device_ok": (I, [I]),
     "sbo_energy_pass": (I, [P, I, I64, I, P, I, I, I, I, I, P, P, P, P, P]),
-    "sbo_energy_recheck": (I, [P, I, I64, I, P, I, I, I, P, P, I64, P, P, P, P]),
+    "sbo_energy_recheck": (I, [P, I, I64, I, P, I, I, I, I, P, P, I64, P, P, P, P]),
     "sbo_tc_padded_rows": (I64, [I64]),
     "sbo_tc_split_signals": (I, [P, I, I64, I, P, P, P, P]),
     "sbo_tc_split_blocks": (I, [P, I, I, P, P, P, P]),
@@ -37,7 +37,7 @@ _SIGS = {
     "sbo_outer_segments": (I, [P, I, I, P, P, P, P, I64, I, I64, P, P, P, P]),
     "sbo_reduce_segments": (I, [P, P, P, I64, I, I, P, P]),
     "sbo_round_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, P, P]),
-    "sbo_residual_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, P, P]),
+    "sbo_residual_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, P, P, P]),
     "sbo_gram_workspace_bytes": (SZ, [I64, I, I]),
     "sbo_gram": (I, [P, I, I, P, I64, I, P, P, SZ, P]),
     "sbo_select_top": (I, [P, I64, I, I, I64, P, P, P]),

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
     const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
     const double* __restrict__ blocks, int block_override, int k, double* partial,
-    double* rest_sq) {
+    double* rest_sq, int kind, double* score) {
   constexpr int NB = Stage<TY>::NB, YLD = Stage<TY>::YLD;
   if (static_cast<int>(blockIdx.x) >= *nseg) return;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       if (mag(u) >= tk && mag(u) >= 0.0f) mask |= 1u << u;
     // float32 ties at the threshold: the warp re-decides those signals exactly
     unsigned need = __ballot_sync(0xffffffffu, act && !(tk > tk1) && t4 == 0);
-    double rest = -1.0;  // < 0: not decided by the fallback
+    double rest = -1.0, fscore = 0.0;  // rest < 0: not decided by the fallback
     while (need) {
       const int gg = (__ffs(need) - 1) >> 2;
       need &= need - 1;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
         for (int u = 0; u < 16; ++u) scr[atom_of(u, t4)] = c[u >> 1][u & 1];
       }
       __syncwarp();
-      const RowPick r = pick_row(scr, p, k, SBO_KIND_SQUARED_SUM);
+      const RowPick r = pick_row(scr, p, k, kind);
       fl[lane] = r.sel & 1u;
       fl[lane + 32] = (r.sel >> 1) & 1u;
       __syncwarp();
@@ -207,22 +207,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
         for (int u = 0; u < 16; ++u)
           if (fl[atom_of(u, t4)]) mask |= 1u << u;
         rest = r.rest_sq;
+        fscore = r.score;
       }
       __syncwarp();
     }
     if constexpr (kResid) {
       // every lane takes part in the quad sum (full-mask shuffles), the
       // fallback's exact value wins where it was computed
-      double d = 0.0;
+      double d = 0.0, e = 0.0;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const double v = c[u >> 1][u & 1];
-        if (!((mask >> u) & 1u) && mag(u) >= 0.0f) d = fma(v, v, d);
+        if ((mask >> u) & 1u) e = kind == SBO_KIND_SQUARED_SUM ? fma(v, v, e) : e + fabs(v);
+        else if (mag(u) >= 0.0f) d = fma(v, v, d);
       }
       d += __shfl_xor_sync(0xffffffffu, d, 1);
       d += __shfl_xor_sync(0xffffffffu, d, 2);
+      e += __shfl_xor_sync(0xffffffffu, e, 1);
+      e += __shfl_xor_sync(0xffffffffu, e, 2);
       if (rest < 0.0) rest = d;
-      if (act && t4 == 0) rest_sq[rows[s]] = rest;
+      else e = fscore;
+      if (act && t4 == 0) {
+        rest_sq[rows[s]] = rest;
+        if (score) score[rows[s]] = e;
+      }
     } else {
       // X = the kept coefficients, zeros elsewhere (fragment layout -> rows of X)
       double* xr = X + s * LD + 2 * t4;
@@ -261,13 +269,13 @@ template <typename TY, bool kResid>
 int launch(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
            const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
            const double* blocks, int block_override, int k, double* partial, double* rest_sq,
-           cudaStream_t st) {
+           int kind, double* score, cudaStream_t st) {
   const Layout<TY> L;
   cudaFuncSetAttribute(k_round64<TY, kResid>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
   k_round64<TY, kResid><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
-      block_override, k, partial, rest_sq);
+      block_override, k, partial, rest_sq, kind, score);
   return check_launch(kResid ? "k_round64<resid>" : "k_round64");
 }
 
@@ -295,24 +303,27 @@ extern "C" int sbo_round_segments(const void* y, int dtype, int p, const int32_t
   return dtype == SBO_F32
              ? r64::launch<float, false>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
                                          blocks, block_override, k, partial, nullptr,
-                                         as_stream(stream))
+                                         SBO_KIND_SQUARED_SUM, nullptr, as_stream(stream))
              : r64::launch<double, false>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
                                           blocks, block_override, k, partial, nullptr,
-                                          as_stream(stream));
+                                          SBO_KIND_SQUARED_SUM, nullptr, as_stream(stream));
 }
 
 extern "C" int sbo_residual_segments(const void* y, int dtype, int p, const int32_t* order,
                                      const int32_t* seg_block, const int64_t* seg_lo,
                                      const int64_t* seg_hi, const int32_t* nseg,
-                                     int64_t max_seg, const double* blocks, int s0,
-                                     double* rest_sq, void* stream) {
+                                     int64_t max_seg, const double* blocks, int s0, int kind,
+                                     double* rest_sq, double* score, void* stream) {
   if (int rc = r64::check(dtype, p, s0)) return rc;
   if (!rest_sq) return fail(SBO_EINVAL, "rest_sq is required");
+  if (kind != SBO_KIND_SQUARED_SUM && kind != SBO_KIND_ABS_SUM) return fail(SBO_EINVAL, "bad kind");
   if (max_seg <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32
              ? r64::launch<float, true>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
-                                        blocks, -1, k, nullptr, rest_sq, as_stream(stream))
+                                        blocks, -1, k, nullptr, rest_sq, kind, score,
+                                        as_stream(stream))
              : r64::launch<double, true>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
-                                         blocks, -1, k, nullptr, rest_sq, as_stream(stream));
+                                         blocks, -1, k, nullptr, rest_sq, kind, score,
+                                         as_stream(stream));
 }

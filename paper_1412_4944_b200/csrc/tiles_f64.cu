@@ -496,47 +496,71 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
   }
 }
 
-// P_b = sum of block b's segment partials, in segment order
-__global__ void k_reduce_segments(const double* __restrict__ partial,
-                                  const int32_t* __restrict__ seg_block,
-                                  const int32_t* __restrict__ nseg, int K, int p, double* P) {
+// P_b = sum of block b's segment partials.  A CTA owns 32 consecutive elements;
+// its 8 warps take the segments s0 + w, s0 + w + 8, ... (coalesced 256-B rows),
+// and the 8 slice sums are added in slice order: a fixed summation order, so the
+// result is deterministic, with 8x the memory-level parallelism of one thread
+// per element.
+__global__ void __launch_bounds__(256) k_reduce_segments(const double* __restrict__ partial,
+                                                        const int32_t* __restrict__ seg_block,
+                                                        const int32_t* __restrict__ nseg, int K,
+                                                        int p, double* P) {
+  __shared__ double part[8][33];
+  __shared__ int range[2];
   const int b = blockIdx.y;
   const int64_t pp = static_cast<int64_t>(p) * p;
-  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int n = *nseg;
-  // segments are sorted by block: binary-search block b's range [s0, s1)
-  int s0 = 0, s1 = n;
-  if (seg_block) {
-    int a = 0, z = n;
-    while (a < z) {
-      const int mid = (a + z) >> 1;
-      if (seg_block[mid] < b) a = mid + 1;
-      else z = mid;
+  const int el = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * 32 + el;
+  if (threadIdx.x == 0) {
+    const int n = *nseg;
+    // segments are sorted by block: binary-search block b's range [s0, s1)
+    int s0 = 0, s1 = n;
+    if (seg_block) {
+      int a = 0, z = n;
+      while (a < z) {
+        const int mid = (a + z) >> 1;
+        if (seg_block[mid] < b) a = mid + 1;
+        else z = mid;
+      }
+      s0 = a;
+      z = n;
+      while (a < z) {
+        const int mid = (a + z) >> 1;
+        if (seg_block[mid] <= b) a = mid + 1;
+        else z = mid;
+      }
+      s1 = a;
+    } else if (b != 0) {
+      s1 = 0;
     }
-    s0 = a;
-    z = n;
-    while (a < z) {
-      const int mid = (a + z) >> 1;
-      if (seg_block[mid] <= b) a = mid + 1;
-      else z = mid;
-    }
-    s1 = a;
-  } else if (b != 0) {
-    s1 = 0;
+    range[0] = s0;
+    range[1] = s1;
   }
-  if (e >= pp) return;
-  // loads batched 8 deep (independent), summed strictly in segment order
+  __syncthreads();
+  const int s0 = range[0], s1 = range[1];
   double acc = 0.0;
-  int s = s0;
-  for (; s + 8 <= s1; s += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcs(partial + (s + u) * pp + e);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc += v[u];
+  if (e < pp) {
+    int s = s0 + sl;
+    for (; s + 24 < s1; s += 32) {  // 4 independent loads in flight
+      const double v0 = __ldcs(partial + static_cast<int64_t>(s) * pp + e);
+      const double v1 = __ldcs(partial + static_cast<int64_t>(s + 8) * pp + e);
+      const double v2 = __ldcs(partial + static_cast<int64_t>(s + 16) * pp + e);
+      const double v3 = __ldcs(partial + static_cast<int64_t>(s + 24) * pp + e);
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; s < s1; s += 8) acc += __ldcs(partial + static_cast<int64_t>(s) * pp + e);
   }
-  for (; s < s1; ++s) acc += __ldcs(partial + s * pp + e);
-  P[b * pp + e] = acc;
+  part[sl][el] = acc;
+  __syncthreads();
+  if (sl == 0 && e < pp) {
+    double t = part[0][el];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t += part[w][el];
+    P[b * pp + e] = t;
+  }
 }
 
 // Gram partials over chunks of a member list, then the ordered reduction
@@ -625,18 +649,20 @@ extern "C" int sbo_energy_pass(const void* y, int dtype, int64_t m, int p, const
 }
 
 extern "C" int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p,
-                                  const double* blocks, int K, int s0, int kind,
+                                  const double* blocks, int b0, int K, int s0, int kind,
                                   const int32_t* list, const int32_t* nlist, int64_t max_list,
                                   int32_t* best, double* score, double* residual_sq,
                                   void* stream) {
   if (int rc = check_common(dtype, p, s0)) return rc;
   if (K < 1 || !list || !nlist) return fail(SBO_EINVAL, "recheck needs K >= 1 and a list");
+  if (b0 < 0 || b0 >= K) return fail(SBO_EINVAL, "recheck needs 0 <= b0 < K");
   if (max_list <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
+  const int acc = b0 > 0 ? 1 : 0;
   return dtype == SBO_F32
-             ? energy_impl<float>(y, m, p, blocks, 0, K, k, kind, 0, list, nlist, max_list,
+             ? energy_impl<float>(y, m, p, blocks, b0, K, k, kind, acc, list, nlist, max_list,
                                   best, score, residual_sq, nullptr, as_stream(stream))
-             : energy_impl<double>(y, m, p, blocks, 0, K, k, kind, 0, list, nlist, max_list,
+             : energy_impl<double>(y, m, p, blocks, b0, K, k, kind, acc, list, nlist, max_list,
                                    best, score, residual_sq, nullptr, as_stream(stream));
 }
 
@@ -679,7 +705,7 @@ extern "C" int sbo_reduce_segments(const double* partial, const int32_t* seg_blo
   if (K < 1 || p < 1) return fail(SBO_EINVAL, "bad reduce shape");
   (void)max_seg;
   const int64_t pp = static_cast<int64_t>(p) * p;
-  dim3 grid(static_cast<unsigned>(ceil_div(pp, 256)), static_cast<unsigned>(K));
+  dim3 grid(static_cast<unsigned>(ceil_div(pp, 32)), static_cast<unsigned>(K));
   k_reduce_segments<<<grid, 256, 0, as_stream(stream)>>>(partial, seg_block, nseg, K, p, P);
   return check_launch("k_reduce_segments");
 }
@@ -712,7 +738,7 @@ extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members,
                                                  nullptr, 1, partial, st);
   if (rc) return rc;
   const int64_t pp = static_cast<int64_t>(p) * p;
-  k_reduce_segments<<<dim3(static_cast<unsigned>(ceil_div(pp, 256)), 1), 256, 0, st>>>(
+  k_reduce_segments<<<dim3(static_cast<unsigned>(ceil_div(pp, 32)), 1), 256, 0, st>>>(
       partial, nullptr, ns, 1, p, G);
   return check_launch("k_reduce_segments(gram)");
 }

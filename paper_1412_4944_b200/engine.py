@@ -299,8 +299,11 @@ class Engine:
                        s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
                        self.flags.data_ptr(), self.nflag.data_ptr(), self.stream,
                        units=self.m * (b1 - b0))
+            # incremental (accumulate): only the appended blocks are re-decided, against
+            # the exact score / residual the previous full representation stored
             self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
-                       self.p, self.blocks.data_ptr(), b1, self.s0, self.kind,
+                       self.p, self.blocks.data_ptr(), b0 if accumulate else 0, b1, self.s0,
+                       self.kind,
                        self.flags.data_ptr(), self.nflag.data_ptr(), self.m, s.best.data_ptr(),
                        s.score.data_ptr(), s.residual.data_ptr(), self.stream)
             self.flag_counts.append(self.nflag.clone())
@@ -448,11 +451,13 @@ class Engine:
                 self._call("sbo_residual_segments", self.sig.y.data_ptr(), self.sig.code,
                            self.p, g.perm.data_ptr(), g.seg_block.data_ptr(),
                            g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(),
-                           g.max_seg, self.blocks.data_ptr(), self.s0,
-                           self.state.residual.data_ptr(), self.stream, units=self.m)
+                           g.max_seg, self.blocks.data_ptr(), self.s0, self.kind,
+                           self.state.residual.data_ptr(), self.state.score.data_ptr(),
+                           self.stream, units=self.m)
             else:
                 ld = max(self.m, 1)
-                self.code(g.perm, g, -1, True, ld, None, None, None, self.state.residual)
+                self.code(g.perm, g, -1, True, ld, None, None, self.state.score,
+                          self.state.residual)
         self.residual()
 
     def rmse(self) -> float:
