@@ -52,56 +52,83 @@ __device__ __forceinline__ void rotation(double al, double be, double ga, double
   s = c * t;
 }
 
-// p = 64 specialization: 32 column pairs per step, 8 lanes per pair, lane lg
-// owns rows lg + 8u; the round-robin schedule advances incrementally and the
-// pair's rows stay in registers between the dot products and the rotation.
+// p = 64 specialization: 32 column pairs per step.  A half-warp (16 lanes) owns a
+// pair, so each shared-memory access reads 16 consecutive rows of ONE column —
+// conflict-free whatever the columns (8 lanes per pair put 4 columns of equal
+// bank alignment in a warp's wavefront); every thread handles pairs q and
+// q + 16 (rows lg + 16u), which also gives two independent chains.  The
+// round-robin schedule advances incrementally.
+template <int NT>
 __device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) {
-  constexpr int N = 64;
-  const int tid = threadIdx.x, q = tid >> 3, lg = tid & 7;
+  static_assert(NT == 256 || NT == 512, "256 threads: 2 pairs each; 512: 1 pair each");
+  constexpr int N = 64, NP = NT == 256 ? 2 : 1;
+  const int tid = threadIdx.x, q = tid >> 4, lg = tid & 15;
   const double tol2 = DBL_EPSILON * DBL_EPSILON;
   const double conv = 4.0 * 8.0 * DBL_EPSILON, conv2 = conv * conv;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     if (tid == 0) *flag = 0;
     __syncthreads();
-    int i = q, j = q == 0 ? N - 1 : N - 1 - q;  // step 0 of the tournament
+    // step 0 of the tournament for pairs q and (256 threads) q + 16
+    int i0 = q, j0 = q == 0 ? N - 1 : N - 1 - q;
+    int i1 = q + 16, j1 = N - 1 - (q + 16);
     for (int step = 0; step < N - 1; ++step) {
-      double* ai = A + i * N + lg;
-      double* aj = A + j * N + lg;
-      double x[8], y[8], al = 0.0, be = 0.0, ga = 0.0;
+      double* ai[2] = {A + i0 * N + lg, A + i1 * N + lg};
+      double* aj[2] = {A + j0 * N + lg, A + j1 * N + lg};
+      double x[2][4], y[2][4], al[2], be[2], ga[2];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        x[u] = ai[8 * u];
-        y[u] = aj[8 * u];
-        al = fma(x[u], x[u], al);
-        be = fma(y[u], y[u], be);
-        ga = fma(x[u], y[u], ga);
-      }
+      for (int h = 0; h < NP; ++h) {
+        al[h] = be[h] = ga[h] = 0.0;
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        al += __shfl_xor_sync(0xffffffffu, al, o);
-        be += __shfl_xor_sync(0xffffffffu, be, o);
-        ga += __shfl_xor_sync(0xffffffffu, ga, o);
-      }
-      const double g2 = ga * ga, ab = al * be;
-      if (al > 0.0 && be > 0.0 && g2 > tol2 * ab) {
-        double c, s;
-        rotation(al, be, ga, c, s);
-        double* vi = V + i * N + lg;
-        double* vj = V + j * N + lg;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          ai[8 * u] = c * x[u] - s * y[u];
-          aj[8 * u] = s * x[u] + c * y[u];
-          const double vu = vi[8 * u], vw = vj[8 * u];
-          vi[8 * u] = c * vu - s * vw;
-          vj[8 * u] = s * vu + c * vw;
+        for (int u = 0; u < 4; ++u) {
+          x[h][u] = ai[h][16 * u];
+          y[h][u] = aj[h][16 * u];
         }
-        if (lg == 0 && g2 > conv2 * ab) *flag = 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          al[h] = fma(x[h][u], x[h][u], al[h]);
+          be[h] = fma(y[h][u], y[h][u], be[h]);
+          ga[h] = fma(x[h][u], y[h][u], ga[h]);
+        }
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+#pragma unroll
+        for (int h = 0; h < NP; ++h) {
+          al[h] += __shfl_xor_sync(0xffffffffu, al[h], o);
+          be[h] += __shfl_xor_sync(0xffffffffu, be[h], o);
+          ga[h] += __shfl_xor_sync(0xffffffffu, ga[h], o);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < NP; ++h) {
+        const double g2 = ga[h] * ga[h], ab = al[h] * be[h];
+        if (al[h] > 0.0 && be[h] > 0.0 && g2 > tol2 * ab) {
+          double c, sn;
+          rotation(al[h], be[h], ga[h], c, sn);
+          double* vi = V + (h ? i1 : i0) * N + lg;
+          double* vj = V + (h ? j1 : j0) * N + lg;
+          double vx[4], vy[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            vx[u] = vi[16 * u];
+            vy[u] = vj[16 * u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ai[h][16 * u] = c * x[h][u] - sn * y[h][u];
+            aj[h][16 * u] = sn * x[h][u] + c * y[h][u];
+            vi[16 * u] = c * vx[u] - sn * vy[u];
+            vj[16 * u] = sn * vx[u] + c * vy[u];
+          }
+          if (lg == 0 && g2 > conv2 * ab) *flag = 1;
+        }
       }
       __syncthreads();
       // next step: i, j advance by one modulo 63 (slot 0 keeps j = 63)
-      i = (i == N - 2) ? 0 : i + 1;
-      if (q != 0) j = (j == N - 2) ? 0 : j + 1;
+      i0 = (i0 == N - 2) ? 0 : i0 + 1;
+      if (q != 0) j0 = (j0 == N - 2) ? 0 : j0 + 1;
+      i1 = (i1 == N - 2) ? 0 : i1 + 1;
+      j1 = (j1 == N - 2) ? 0 : j1 + 1;
     }
     if (*flag == 0) return sweep + 1;
     __syncthreads();
@@ -112,7 +139,8 @@ __device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) 
 // Runs the sweeps on A (p x p, col-major) accumulating V.  Returns the sweep
 // count, or -1 when kMaxSweeps is exhausted.  All threads of the CTA call it.
 __device__ __forceinline__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
-  if (rows == 64 && p == 64 && blockDim.x == 256) return jacobi_sweeps64(A, V, flag);
+  if (rows == 64 && p == 64 && blockDim.x == 256) return jacobi_sweeps64<256>(A, V, flag);
+  if (rows == 64 && p == 64 && blockDim.x == 512) return jacobi_sweeps64<512>(A, V, flag);
   const int n = p + (p & 1);
   const int npairs = n >> 1;
   int g = 32;
@@ -213,6 +241,7 @@ __device__ __forceinline__ void column_order(const double* A, int rows, int p, d
 }
 
 // orthonormality defect of a row-major p x p matrix (CTA-wide, deterministic)
+template <int NT = kJacobiThreads>
 __device__ __forceinline__ double defect_of(const double* Q, int p, double* red) {
   double acc = 0.0;
   for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
@@ -222,7 +251,7 @@ __device__ __forceinline__ double defect_of(const double* Q, int p, double* red)
     g -= (a == b) ? 1.0 : 0.0;
     acc = fma(g, g, acc);
   }
-  return sqrt(block_sum<kJacobiThreads>(acc, red));
+  return sqrt(block_sum<NT>(acc, red));
 }
 
 // ---------------------------------------------------------------------------
@@ -644,8 +673,8 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
 }
 
 // ---------------------------------------------------------------------------
-template <bool SMEM>
-__global__ void __launch_bounds__(kJacobiThreads) k_init_block(
+template <bool SMEM, int NT>
+__global__ void __launch_bounds__(NT) k_init_block(
     const double* __restrict__ G, int p, int64_t ncols, const double* __restrict__ draws,
     int ndraws, double* Q, int32_t* rank_out, int32_t* status, double* ws, int use_smem) {
   const int64_t pp = static_cast<int64_t>(p) * p;
@@ -717,14 +746,14 @@ __global__ void __launch_bounds__(kJacobiThreads) k_init_block(
         const double* w = U + static_cast<int64_t>(l) * p;
         double dd = 0.0;
         for (int r = threadIdx.x; r < p; r += blockDim.x) dd = fma(w[r], u[r], dd);
-        dd = block_sum<kJacobiThreads>(dd, S.red);
+        dd = block_sum<NT>(dd, S.red);
         for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] -= dd * w[r];
         __syncthreads();
       }
     }
     double nn = 0.0;
     for (int r = threadIdx.x; r < p; r += blockDim.x) nn = fma(u[r], u[r], nn);
-    nn = sqrt(block_sum<kJacobiThreads>(nn, S.red));
+    nn = sqrt(block_sum<NT>(nn, S.red));
     if (nn < 1e-8) continue;
     for (int r = threadIdx.x; r < p; r += blockDim.x) u[r] /= nn;
     __syncthreads();
@@ -736,7 +765,7 @@ __global__ void __launch_bounds__(kJacobiThreads) k_init_block(
     Q[e] = U[static_cast<int64_t>(i) * p + k];
   }
   __syncthreads();
-  const double df = defect_of(Q, p, S.red);
+  const double df = defect_of<NT>(Q, p, S.red);
   if (threadIdx.x == 0) {
     if (rank_out) {
       rank_out[0] = rank;
@@ -821,12 +850,19 @@ extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const doubl
     return fail(SBO_EINVAL, "init workspace too small");
   const size_t dyn = smem ? init_smem_bytes(p) : 0;
   if (smem) {
-    cudaFuncSetAttribute(k_init_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(dyn));
-    k_init_block<true><<<1, kJacobiThreads, dyn, as_stream(stream)>>>(
-        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
+    if (p == 64) {  // 512 threads: one column pair per half-warp (jacobi_sweeps64)
+      cudaFuncSetAttribute(k_init_block<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(dyn));
+      k_init_block<true, 512><<<1, 512, dyn, as_stream(stream)>>>(
+          G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
+    } else {
+      cudaFuncSetAttribute(k_init_block<true, kJacobiThreads>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+      k_init_block<true, kJacobiThreads><<<1, kJacobiThreads, dyn, as_stream(stream)>>>(
+          G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
+    }
   } else {
-    k_init_block<false><<<1, kJacobiThreads, 0, as_stream(stream)>>>(
+    k_init_block<false, kJacobiThreads><<<1, kJacobiThreads, 0, as_stream(stream)>>>(
         G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 0);
   }
   return check_launch("k_init_block");

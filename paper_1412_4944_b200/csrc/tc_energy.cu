@@ -215,6 +215,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           // network drops (+ the tail of the top-G list beyond k): no S - kept cancellation
           float dropped = 0.0f;
           if constexpr (ABS) topk::top_of_64<G>(v);
+          else if (ksel == G) dropped = topk::top_of_64_dropped<G, false>(v);  // order unused
           else dropped = topk::top_of_64_dropped<G>(v);
           float kept = 0.0f, e = 0.0f;
 #pragma unroll

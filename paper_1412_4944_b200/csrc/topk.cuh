@@ -25,9 +25,23 @@ __device__ __forceinline__ void merge_desc(float* v) {
   }
 }
 
-// any N (power of two) -> sorted descending (bitonic sort)
+// 8 values -> sorted descending with the optimal 19-comparator network (depth 6)
+__device__ __forceinline__ void sort8_desc(float* v) {
+  cx(v[0], v[2]); cx(v[1], v[3]); cx(v[4], v[6]); cx(v[5], v[7]);
+  cx(v[0], v[4]); cx(v[1], v[5]); cx(v[2], v[6]); cx(v[3], v[7]);
+  cx(v[0], v[1]); cx(v[2], v[3]); cx(v[4], v[5]); cx(v[6], v[7]);
+  cx(v[2], v[4]); cx(v[3], v[5]);
+  cx(v[1], v[4]); cx(v[3], v[6]);
+  cx(v[1], v[2]); cx(v[3], v[4]); cx(v[5], v[6]);
+}
+
+// any N (power of two) -> sorted descending (bitonic sort; 8 uses sort8_desc)
 template <int N>
 __device__ __forceinline__ void sort_desc(float* v) {
+  if constexpr (N == 8) {
+    sort8_desc(v);
+    return;
+  }
 #pragma unroll
   for (int size = 2; size <= N; size <<= 1) {
 #pragma unroll
@@ -72,7 +86,9 @@ __device__ __forceinline__ void top_of_64(float* v) {
 // As top_of_64, also summing every value the network discards (each merge
 // keeps max(a_i, b_{G-1-i}) and drops the min): sum(v) = sum(top) + dropped,
 // with dropped accumulated from the small values themselves (no cancellation).
-template <int G>
+// SORTED = false: the final merge leaves v[0..G) as the top-G SET (bitonic, not
+// sorted) — enough when every one of them is kept (k == G).
+template <int G, bool SORTED = true>
 __device__ __forceinline__ float top_of_64_dropped(float* v) {
   float dropped = 0.0f;
 #pragma unroll
@@ -89,7 +105,7 @@ __device__ __forceinline__ float top_of_64_dropped(float* v) {
         a[i] = fmaxf(x, y);
         dropped += fminf(x, y);
       }
-      merge_desc<G>(a);
+      if (SORTED || 2 * step < 64) merge_desc<G>(a);
     }
   }
   return dropped;
