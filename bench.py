@@ -122,36 +122,79 @@ def peaks():
 #          sparse outer product 2 p k — the reference's train_onb round
 #   tc     (sbo_tc_energy, unit = signal x block): projection 2p^2
 #   code   (sbo_code_segments, unit = signal): projection 2p^2
-FP64_PEAK_TFLOPS = 33.0  # measured FFMA.F64 throughput on this pool (profiles/fp64_micro.txt)
+FP64_PEAK_TFLOPS = 33.0       # measured DFMA throughput on this pool (profiles/fp64_micro.txt)
+DMMA_PEAK_TFLOPS = 37.0       # measured float64 tensor-core (DMMA m8n8k4) throughput, same file
 
 
 def kernel_families(timer, p, k):
-    fam = {"sbo_round_segments": ("k_round_f64", 2 * p * p + 2 * p * k, "fp64 tensor cores (DMMA)"),
-           "sbo_tc_energy": ("k_energy_tc", 2 * p * p, "tcgen05 split-fp16"),
-           "sbo_code_segments": ("k_code_f64", 2 * p * p, "fp64 CUDA cores"),
-           "sbo_residual_segments": ("k_round_f64<resid>", 2 * p * p, "fp64 tensor cores (DMMA)"),
-           "sbo_polar": ("k_polar_ns", 0, "fp64 CUDA cores (latency)"),
-           "sbo_energy_recheck": ("k_energy_f64 recheck", 0, "fp64 CUDA cores")}
+    """Per ABI-call family: launches, time, algorithmic flop rate (the reference's
+    work: sparse outer product 2pk) and implemented flop rate (what the kernel
+    issues: dense DMMA outer product 2p^2; three fp16 products in the split)."""
+    fam = {"sbo_round_segments": ("k_round64", 2 * p * p + 2 * p * k, 4 * p * p,
+                                  "fp64 tensor cores (DMMA)"),
+           "sbo_tc_energy": ("k_energy_tc", 2 * p * p, 6 * p * p, "tcgen05 split-fp16"),
+           "sbo_code_segments": ("k_code_f64", 2 * p * p, 2 * p * p, "fp64 CUDA cores"),
+           "sbo_residual_segments": ("k_round64<resid>", 2 * p * p, 2 * p * p,
+                                     "fp64 tensor cores (DMMA)"),
+           "sbo_polar": ("k_polar_ns_cluster", 0, 0, "fp64 tensor cores (DMMA), latency"),
+           "sbo_energy_recheck": ("k_energy_f64 recheck", 0, 0, "fp64 tensor cores (DMMA)")}
     out = {}
-    for name, (kname, fpu, pipe) in fam.items():
+    for name, (kname, fpu, ipu, pipe) in fam.items():
         ev = [(u, e0.elapsed_time(e1)) for (n, u, e0, e1) in timer if n == name]
         if not ev:
             continue
         ms = sum(t for _, t in ev)
         units = sum(u for u, _ in ev)
         out[kname] = {"launches": len(ev), "ms_total": ms, "units": units,
-                      "flop_per_unit": fpu, "pipe": pipe,
-                      "tflops": (fpu * units / (ms * 1e-3) / 1e12) if fpu and ms else None}
+                      "flop_per_unit": fpu, "implemented_flop_per_unit": ipu, "pipe": pipe,
+                      "tflops": (fpu * units / (ms * 1e-3) / 1e12) if fpu and ms else None,
+                      "implemented_tflops": (ipu * units / (ms * 1e-3) / 1e12) if ipu and ms
+                      else None}
     return out
+
+
+def ncu_traffic(kname):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kname` from the
+    newest committed ncu --set full summary (profiles/*_ncu_summary.txt), or None."""
+    import glob
+    files = sorted(glob.glob(str(ROOT / "profiles" / "*_ncu_summary.txt")))
+    want = {"k_round64": "k_round64<float, 0>", "k_round64<resid>": "k_round64<float, 1>",
+            "k_energy_tc": "k_energy_tc<"}.get(kname)
+    if not files or not want:
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    cur, total, path = None, {}, files[-1]
+    for line in open(path):
+        if line.startswith("=="):
+            cur = want in line
+            total = {} if cur else total
+            continue
+        f = line.split()
+        if cur and len(f) >= 3 and f[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total[f[0]] = float(f[1]) * scale.get(f[2], 1.0)
+        if cur and len(total) == 2:
+            return {"bytes_per_launch": sum(total.values()), "source": os.path.basename(path)}
+    return None
 
 
 def roofline_of(kname, info, bf16, src, steps):
     achieved = info["tflops"] or 0.0
+    tr = ncu_traffic(kname)
     return {"kernel": kname, "bound": "tensor", "achieved": achieved, "peak": bf16,
-            "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
+            "unit": "TFLOP/s", "frac": achieved / bf16,
+            "traffic": tr["bytes_per_launch"] if tr else None,
+            "traffic_source": tr["source"] if tr else None,
             "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json)",
             "fp64_peak": FP64_PEAK_TFLOPS,
             "frac_of_fp64_peak": achieved / FP64_PEAK_TFLOPS if "fp64" in info["pipe"] else None,
+            "dmma_peak": DMMA_PEAK_TFLOPS,
+            "frac_of_dmma_peak": achieved / DMMA_PEAK_TFLOPS if "DMMA" in info["pipe"] else None,
+            "implemented_tflops": info.get("implemented_tflops"),
+            "implemented_frac_of_dmma_peak": (info["implemented_tflops"] / DMMA_PEAK_TFLOPS
+                                              if "DMMA" in info["pipe"]
+                                              and info.get("implemented_tflops") else None),
+            "note": ("float64 kernel: the bf16 tensor peak is not its ceiling; the measured "
+                     "float64 tensor-core (DMMA) peak is" if "fp64" in info["pipe"] else None),
             "pipe": info["pipe"], "launches_per_step": info["launches"] / steps,
             "ms_per_step": info["ms_total"] / steps,
             "algorithmic": f"{info['flop_per_unit']} flop per unit, {info['units'] // steps} "
