@@ -124,17 +124,36 @@ __global__ void __launch_bounds__(kGroupTile) k_group_scatter(const int32_t* __r
                                                              const int64_t* __restrict__ bounds,
                                                              int32_t* perm) {
   __shared__ WarpRuns runs[kGroupTile / 32];
+  __shared__ int before[kGroupTile / 32][65];  // K <= 64: per-warp exclusive block counts
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kGroupTile + threadIdx.x;
   const bool valid = j < m;
   const int b = valid ? best[j] : -1;
   int r;
-  const int w = threadIdx.x >> 5;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   warp_runs(b, valid, &runs[w], &r);
-  __syncthreads();
-  if (!valid) return;
-  for (int v = 0; v < w; ++v)
-    for (int e = 0; e < runs[v].n; ++e)
-      if (runs[v].val[e] == b) r += runs[v].cnt[e];
+  if (K <= 64) {
+    for (int e = threadIdx.x; e < (kGroupTile / 32) * 64; e += kGroupTile) before[e >> 6][e & 63] = 0;
+    __syncthreads();
+    if (l < runs[w].n) before[w][runs[w].val[l]] = runs[w].cnt[l];
+    __syncthreads();
+    if (threadIdx.x < K) {  // exclusive scan over warps, one block per thread
+      int acc = 0;
+      for (int v = 0; v < kGroupTile / 32; ++v) {
+        const int c = before[v][threadIdx.x];
+        before[v][threadIdx.x] = acc;
+        acc += c;
+      }
+    }
+    __syncthreads();
+    if (!valid) return;
+    r += before[w][b];
+  } else {
+    __syncthreads();
+    if (!valid) return;
+    for (int v = 0; v < w; ++v)
+      for (int e = 0; e < runs[v].n; ++e)
+        if (runs[v].val[e] == b) r += runs[v].cnt[e];
+  }
   perm[bounds[b] + off[static_cast<int64_t>(blockIdx.x) * K + b] + r] = static_cast<int32_t>(j);
 }
 
@@ -164,20 +183,32 @@ __global__ void k_key_hist(const double* __restrict__ r, int64_t m, const Select
                         static_cast<unsigned long long>(h[i]));
 }
 
-__global__ void k_key_pick(SelectState* st, long long* hist, int shift) {
-  if (threadIdx.x == 0) {
-    long long need = st->need, cum = 0;
-    int d = 0;
-    for (d = 255; d >= 0; --d) {
-      if (cum + hist[d] >= need) break;
-      cum += hist[d];
-    }
-    if (d < 0) d = 0;  // unreachable when need <= count
-    st->need = need - cum;
+// the digit d of the need-th largest key: with suffix sums S[d] = sum_{d' >= d} h[d'],
+// the largest d with S[d] >= need (256 threads, one bin each, block scan)
+__global__ void __launch_bounds__(256) k_key_pick(SelectState* st, long long* hist, int shift) {
+  __shared__ long long wsum[8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int d = 255 - t;  // thread t owns bin 255 - t: a prefix over t is a suffix over d
+  const long long v = hist[d];
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long n = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += n;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  long long before = 0;
+  for (int i = 0; i < w; ++i) before += wsum[i];
+  const long long incl = x + before;  // S[d]
+  const long long excl = incl - v;    // S[d + 1]
+  const long long need = st->need;
+  __syncthreads();  // every thread has read st->need
+  if (incl >= need && excl < need) {
+    st->need = need - excl;
     st->prefix |= static_cast<unsigned long long>(d) << shift;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  hist[d] = 0;
 }
 
 // per-tile (greater, equal) counts against the threshold
