@@ -172,10 +172,19 @@ __global__ void k_key_hist(const double* __restrict__ r, int64_t m, const Select
   __syncthreads();
   const unsigned long long prefix = st ? st->prefix : prefix_arg;
   const int hs = shift + 8;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long key = key_of(r[j]);
-    if (hs >= 64 || (key >> hs) == (prefix >> hs)) atomicAdd(&h[(key >> shift) & 255u], 1u);
+  const int lane = threadIdx.x & 31;
+  // warp-aggregated: keys share few digits (the high bytes of similar floats), so
+  // one shared atomic per distinct digit per warp instead of one per key
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < m;
+       base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = base + threadIdx.x;
+    int bin = -1;
+    if (j < m) {
+      const unsigned long long key = key_of(r[j]);
+      if (hs >= 64 || (key >> hs) == (prefix >> hs)) bin = static_cast<int>((key >> shift) & 255u);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && __ffs(peers) - 1 == lane) atomicAdd(&h[bin], static_cast<unsigned>(__popc(peers)));
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += blockDim.x)

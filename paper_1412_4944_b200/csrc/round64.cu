@@ -67,6 +67,14 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;"); }
 
+__device__ __forceinline__ float select_f(bool c, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}"
+      : "=f"(r)
+      : "f"(a), "f"(b), "r"(static_cast<int>(c)));
+  return r;
+}
+
 __device__ __forceinline__ int atom_of(int u, int t4) { return 8 * (u >> 1) + 2 * t4 + (u & 1); }
 
 template <typename TY, bool kResid>
@@ -176,11 +184,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       for (int u = 0; u < 16; ++u) other[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
       topk::merge_top<16>(srt, other);
     }
+    // the k-th / (k+1)-th largest by register selects (a plain srt[k - 1] with
+    // runtime k would go through local memory)
     float tk = srt[0], tk1 = srt[1];
 #pragma unroll
     for (int u = 1; u < 16; ++u) {
-      if (u == k - 1) tk = srt[u];
-      if (u == k) tk1 = srt[u];
+      tk = select_f(u == k - 1, srt[u], tk);
+      tk1 = select_f(u == k, srt[u], tk1);
     }
     uint32_t mask = 0u;
 #pragma unroll
