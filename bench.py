@@ -137,7 +137,9 @@ def kernel_families(timer, p, k):
            "sbo_residual_segments": ("k_round64<resid>", 2 * p * p, 2 * p * p,
                                      "fp64 tensor cores (DMMA)"),
            "sbo_polar": ("k_polar_ns_cluster", 0, 0, "fp64 tensor cores (DMMA), latency"),
-           "sbo_energy_recheck": ("k_energy_f64 recheck", 0, 0, "fp64 tensor cores (DMMA)")}
+           "sbo_energy_recheck": ("k_energy_f64 recheck", 0, 0, "fp64 tensor cores (DMMA)"),
+           "sbo_energy_recheck_cand": ("k_energy_f64 recheck (candidates)", 0, 0,
+                                       "fp64 tensor cores (DMMA)")}
     out = {}
     for name, (kname, fpu, ipu, pipe) in fam.items():
         ev = [(u, e0.elapsed_time(e1)) for (n, u, e0, e1) in timer if n == name]
@@ -261,7 +263,7 @@ def run_reference(a):
 
 
 # --------------------------------------------------------------------------- GPU
-KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1,
+KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1, "sbo_cand_sort": 3,
                     "sbo_outer_segments": 1, "sbo_reduce_segments": 1, "sbo_polar": 2,
                     "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_sum": 2,
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2}

@@ -502,6 +502,98 @@ extern "C" int sbo_worst_collect(const double* residual_sq, int64_t m, uint64_t 
   return check_launch("k_worst_collect");
 }
 
+// ---------------------------------------------------------------------------
+// ordering of the flagged signals by their two lowest candidate blocks
+// ---------------------------------------------------------------------------
+constexpr int kCandKeys = 32 * 33;
+
+__device__ __forceinline__ int cand_key(uint32_t mask) {
+  const int lo = mask ? __ffs(static_cast<int>(mask)) - 1 : 0;
+  const uint32_t rest = mask & (mask - 1u);
+  const int hi = rest ? __ffs(static_cast<int>(rest)) - 1 : 32;
+  return lo * 33 + hi;
+}
+
+__global__ void k_cand_hist(const int32_t* __restrict__ cand, const int32_t* nflag, int* cnt) {
+  __shared__ int h[kCandKeys];
+  for (int i = threadIdx.x; i < kCandKeys; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int n = *nflag;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[cand_key(static_cast<uint32_t>(cand[i]))], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCandKeys; i += blockDim.x)
+    if (h[i]) atomicAdd(&cnt[i], h[i]);
+}
+
+__global__ void __launch_bounds__(1024) k_cand_scan(int* cnt) {
+  __shared__ int wsum[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  constexpr int PER = (kCandKeys + 1023) / 1024;  // keys per thread (2)
+  int v[PER], tot = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = t * PER + u;
+    v[u] = i < kCandKeys ? cnt[i] : 0;
+    tot += v[u];
+  }
+  int x = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += n;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s2 = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, s2, o);
+      if (lane >= o) s2 += n;
+    }
+    wsum[lane] = s2;
+  }
+  __syncthreads();
+  int off = x - tot + (w > 0 ? wsum[w - 1] : 0);
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = t * PER + u;
+    if (i < kCandKeys) cnt[i] = off;
+    off += v[u];
+  }
+}
+
+__global__ void k_cand_scatter(const int32_t* __restrict__ flags, const int32_t* __restrict__ cand,
+                               const int32_t* nflag, int* off, int32_t* flags_out,
+                               int32_t* cand_out) {
+  const int n = *nflag;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t mk = static_cast<uint32_t>(cand[i]);
+    const int at = atomicAdd(&off[cand_key(mk)], 1);
+    flags_out[at] = flags[i];
+    cand_out[at] = static_cast<int32_t>(mk);
+  }
+}
+
+extern "C" size_t sbo_cand_workspace_bytes(void) { return sizeof(int) * kCandKeys + 64; }
+
+extern "C" int sbo_cand_sort(const int32_t* flags, const int32_t* cand, const int32_t* nflag,
+                             int64_t max_list, int32_t* flags_out, int32_t* cand_out, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (ws_bytes < sbo_cand_workspace_bytes()) return fail(SBO_EINVAL, "cand workspace too small");
+  if (!flags || !cand || !nflag || !flags_out || !cand_out) return fail(SBO_EINVAL, "null list");
+  if (max_list <= 0) return SBO_OK;
+  cudaStream_t st = as_stream(stream);
+  int* cnt = static_cast<int*>(ws);
+  SBO_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * kCandKeys, st));
+  const int grid = static_cast<int>(ceil_div(max_list, 256) < 296 ? ceil_div(max_list, 256) : 296);
+  k_cand_hist<<<grid, 256, 0, st>>>(cand, nflag, cnt);
+  k_cand_scan<<<1, 1024, 0, st>>>(cnt);
+  k_cand_scatter<<<grid, 256, 0, st>>>(flags, cand, nflag, cnt, flags_out, cand_out);
+  return check_launch("k_cand_sort");
+}
+
 extern "C" size_t sbo_sum_workspace_bytes(int64_t n) {
   return sizeof(double) * (ceil_div(n, kSumTile) + 1) + 64;
 }

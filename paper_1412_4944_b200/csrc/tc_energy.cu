@@ -42,6 +42,7 @@ struct Smem {
   uint32_t tmem;
   float x_r1[M], x_r2[M], x_s[M], x_rb[M], x_eb[M];
   int x_b1[M];
+  float x_dec[32][M];  // decision value per (block - b0, signal) for the candidate masks
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 
@@ -79,7 +80,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
             const int16_t* __restrict__ escale, int64_t m, const __half* __restrict__ qh,
             const __half* __restrict__ ql, const int16_t* __restrict__ fscale, int b0, int b1,
             int ksel, int accumulate, int32_t* best, double* score, double* residual,
-            int32_t* flags, int32_t* nflag) {
+            int32_t* flags, int32_t* nflag, int32_t* cand) {
   extern __shared__ unsigned char raw[];
   Smem* S = smem_of(raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -189,6 +190,8 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
       preload(t + gridDim.x, es_next, prev_next);
       float d1 = INFINITY, d2 = INFINITY, rb = 0.0f, eb = 0.0f, snorm = 0.0f;
       int bb = -1;
+      // decision values are kept per block (shared memory) so that the flagged
+      // signals' candidate masks can be formed against the final best
       for (int c = 0; c < nchunks; ++c) {
         const int nb = min(CHUNK, nblk - c * CHUNK);
         sm100::mbar_wait(&S->acc_full[racc.i], racc.ph);
@@ -245,6 +248,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
             d2 = dec;
           }
           snorm = sq;
+          if (cand && b - b0 < 32) S->x_dec[b - b0][row] = dec;
         }
         sm100::tc_fence_before();
         __syncwarp();
@@ -296,7 +300,24 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           score[j] = ABS ? eb : static_cast<double>(snorm) - rb;
           residual[j] = rb;
         }
-        if (flag) flags[atomicAdd(nflag, 1)] = static_cast<int32_t>(j);
+        if (flag) {
+          const int ix = atomicAdd(nflag, 1);
+          flags[ix] = static_cast<int32_t>(j);
+          if (cand) {
+            // candidate blocks: within the certificate's tolerance of the final best
+            // (1 % slack on the bound); all blocks when more than 32
+            uint32_t cmask = 0xFFFFFFFFu;
+            if (nblk <= 32) {
+              cmask = 0u;
+              const float lim = d1 + 1.01f * err(d1);
+              for (int jb = 0; jb < nblk; ++jb) {
+                const float dv = S->x_dec[jb][row];
+                if (dv <= lim + 1.01f * err(dv)) cmask |= 1u << jb;
+              }
+            }
+            cand[ix] = static_cast<int32_t>(cmask);
+          }
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS));
     }
@@ -380,7 +401,7 @@ template <int G, bool ABS>
 int launch_energy(const __half* yh, const __half* yl, const int16_t* es, int64_t m,
                   const __half* qh, const __half* ql, const int16_t* fs, int b0, int b1, int ksel,
                   int accumulate, int32_t* best, double* score, double* residual,
-                  int32_t* flags, int32_t* nflag, cudaStream_t st) {
+                  int32_t* flags, int32_t* nflag, int32_t* cand, cudaStream_t st) {
   auto kern = k_energy_tc<G, ABS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(SMEM_BYTES));
@@ -390,7 +411,7 @@ int launch_energy(const __half* yh, const __half* yl, const int16_t* es, int64_t
   const int64_t ntiles = ceil_div(m, M);
   const int grid = static_cast<int>(ntiles < sms ? ntiles : sms);
   kern<<<grid, THREADS, SMEM_BYTES, st>>>(yh, yl, es, m, qh, ql, fs, b0, b1, ksel, accumulate,
-                                          best, score, residual, flags, nflag);
+                                          best, score, residual, flags, nflag, cand);
   return check_launch("k_energy_tc");
 }
 
@@ -432,7 +453,7 @@ extern "C" int sbo_tc_energy(const void* yhv, const void* ylv, const int16_t* es
                              int64_t m, const void* qhv, const void* qlv,
                              const int16_t* fscale, int b0, int b1, int s0, int kind,
                              int accumulate, int32_t* best, double* score, double* residual,
-                             int32_t* flags, int32_t* nflag, void* stream) {
+                             int32_t* flags, int32_t* nflag, int32_t* cand, void* stream) {
   const __half* yh = static_cast<const __half*>(yhv);
   const __half* yl = static_cast<const __half*>(ylv);
   const __half* qh = static_cast<const __half*>(qhv);
@@ -448,10 +469,10 @@ extern "C" int sbo_tc_energy(const void* yhv, const void* ylv, const int16_t* es
   if (k <= GG)                                                                                \
     return abs ? tc::launch_energy<GG, true>(yh, yl, escale, m, qh, ql, fscale, b0, b1, k,   \
                                              accumulate, best, score, residual, flags, nflag, \
-                                             st)                                              \
+                                             cand, st)                                        \
                : tc::launch_energy<GG, false>(yh, yl, escale, m, qh, ql, fscale, b0, b1, k,  \
                                               accumulate, best, score, residual, flags,       \
-                                              nflag, st);
+                                              nflag, cand, st);
   SBO_TC_CASE(1)
   SBO_TC_CASE(2)
   SBO_TC_CASE(4)

@@ -214,8 +214,9 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
     const TY* __restrict__ y, int64_t m, int p, const double* __restrict__ blocks, int b0,
     int b1, int k, int kind, int accumulate, const int32_t* __restrict__ list,
     const int32_t* __restrict__ nlist, int32_t* best, double* score, double* rest_sq,
-    double* norm_sq) {
+    double* norm_sq, const int32_t* __restrict__ cand) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned tile_cand;  // union of the tile's candidate blocks (bit b - b0)
   const TileLayout L(p);
   double* C = reinterpret_cast<double*>(smem + L.c_off);
   double* sY = reinterpret_cast<double*>(smem + L.y_off);
@@ -245,10 +246,16 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
         brest[threadIdx.x] = 0.0;
       }
     }
+    if (threadIdx.x == 0) tile_cand = cand ? 0u : 0xFFFFFFFFu;
     __syncthreads();
+    if (cand && threadIdx.x < kTile && base + threadIdx.x < count)
+      atomicOr(&tile_cand, static_cast<unsigned>(cand[base + threadIdx.x]));
+    __syncthreads();
+    const unsigned tcand = tile_cand;
     int* fb = bbest + kTile;  // per-signal "needs the exact rank method" marks
     if (p <= 64) stage_y64(y, p, rows, sY);
     for (int b = b0; b < b1; ++b) {
+      if (b - b0 < 32 && !((tcand >> (b - b0)) & 1u)) continue;  // no signal of the tile can win here
       if (p <= 64) {
         __syncthreads();
         stage_q64(blocks + static_cast<int64_t>(b) * p * p, p, sQ);
@@ -583,7 +590,7 @@ template <typename TY>
 int energy_impl(const void* yv, int64_t m, int p, const double* blocks, int b0, int b1, int k,
                 int kind, int accumulate, const int32_t* list, const int32_t* nlist,
                 int64_t max_list, int32_t* best, double* score, double* rest_sq,
-                double* norm_sq, cudaStream_t st) {
+                double* norm_sq, cudaStream_t st, const int32_t* cand = nullptr) {
   const TileLayout L(p);
   cudaFuncSetAttribute(k_energy_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
@@ -592,7 +599,7 @@ int energy_impl(const void* yv, int64_t m, int p, const double* blocks, int b0, 
   if (tiles < 1) tiles = 1;
   k_energy_f64<TY><<<static_cast<unsigned>(tiles), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), m, p, blocks, b0, b1, k, kind, accumulate, list, nlist, best,
-      score, rest_sq, norm_sq);
+      score, rest_sq, norm_sq, cand);
   return check_launch("k_energy_f64");
 }
 
@@ -664,6 +671,23 @@ extern "C" int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p,
                                   best, score, residual_sq, nullptr, as_stream(stream))
              : energy_impl<double>(y, m, p, blocks, b0, K, k, kind, acc, list, nlist, max_list,
                                    best, score, residual_sq, nullptr, as_stream(stream));
+}
+
+extern "C" int sbo_energy_recheck_cand(const void* y, int dtype, int64_t m, int p,
+                                       const double* blocks, int K, int s0, int kind,
+                                       const int32_t* list, const int32_t* cand,
+                                       const int32_t* nlist, int64_t max_list, int32_t* best,
+                                       double* score, double* residual_sq, void* stream) {
+  if (int rc = check_common(dtype, p, s0)) return rc;
+  if (K < 1 || K > 32 || !list || !cand || !nlist)
+    return fail(SBO_EINVAL, "candidate recheck needs 1 <= K <= 32, a list and its masks");
+  if (max_list <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? energy_impl<float>(y, m, p, blocks, 0, K, k, kind, 0, list, nlist, max_list,
+                                  best, score, residual_sq, nullptr, as_stream(stream), cand)
+             : energy_impl<double>(y, m, p, blocks, 0, K, k, kind, 0, list, nlist, max_list,
+                                   best, score, residual_sq, nullptr, as_stream(stream), cand);
 }
 
 extern "C" int sbo_code_segments(const void* y, int dtype, int p, const int32_t* order,

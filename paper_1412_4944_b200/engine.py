@@ -190,6 +190,9 @@ class Engine:
                            torch.zeros(self.m, **f64), torch.zeros(1, **f64))
         self.launches = 0
         self.flag_counts = []
+        # state.score holds exact float64 scores for every signal (set by a full
+        # representation's residual pass); the incremental re-decision needs them
+        self.exact_scores = False
         # tensor-core representation (p = 64): split-fp16 operands, built once
         self.tc = self.p == 64 and os.environ.get("SBO_TC", "1") != "0" and self.m > 0
         if self.tc:
@@ -240,6 +243,7 @@ class Engine:
                             dtype=torch.float64)
         K = t.shape[0]
         self.K = 0
+        self.exact_scores = False
         self.ensure_capacity(K)
         self.blocks[:K].copy_(t.to(self.dev))
         self.reset_rotation(0, K)
@@ -248,7 +252,7 @@ class Engine:
     def snapshot(self) -> dict:
         """Device copy of the iteration-entering state (blocks, assignment)."""
         st = self.state
-        return {"K": self.K, "blocks": self.blocks.clone(),
+        return {"K": self.K, "blocks": self.blocks.clone(), "exact_scores": self.exact_scores,
                 "state": [t.clone() for t in (st.best, st.score, st.norm, st.residual, st.total)]}
 
     def restore(self, snap: dict):
@@ -258,6 +262,7 @@ class Engine:
         for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total), snap["state"]):
             dst.copy_(src)
         self.K = snap["K"]
+        self.exact_scores = snap["exact_scores"]
 
     def reset_rotation(self, b0: int, b1: int):
         """Identity warm start for the polar Jacobi of blocks [b0, b1)."""
@@ -293,20 +298,42 @@ class Engine:
                        self.qh.data_ptr(), self.ql.data_ptr(), self.fscale.data_ptr(),
                        self.stream)
             self.nflag.zero_()
+            # full pass over <= 32 blocks: the flagged signals carry candidate-block
+            # masks; sorted by them, the float64 tiles only visit their union
+            use_cand = not accumulate and b1 - b0 <= 32
+            if use_cand and getattr(self, "cand", None) is None:
+                i32 = dict(dtype=torch.int32, device=self.dev)
+                self.cand = torch.empty(self.m, **i32)
+                self.flags_sorted = torch.empty(self.m, **i32)
+                self.cand_sorted = torch.empty(self.m, **i32)
             self._call("sbo_tc_energy", self.yh.data_ptr(), self.yl.data_ptr(),
                        self.escale.data_ptr(), self.m, self.qh.data_ptr(), self.ql.data_ptr(),
                        self.fscale.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
                        s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
-                       self.flags.data_ptr(), self.nflag.data_ptr(), self.stream,
+                       self.flags.data_ptr(), self.nflag.data_ptr(),
+                       self.cand.data_ptr() if use_cand else None, self.stream,
                        units=self.m * (b1 - b0))
-            # incremental (accumulate): only the appended blocks are re-decided, against
-            # the exact score / residual the previous full representation stored
-            self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
-                       self.p, self.blocks.data_ptr(), b0 if accumulate else 0, b1, self.s0,
-                       self.kind,
-                       self.flags.data_ptr(), self.nflag.data_ptr(), self.m, s.best.data_ptr(),
-                       s.score.data_ptr(), s.residual.data_ptr(), self.stream)
-            self.flag_counts.append(self.nflag.clone())
+            if use_cand:
+                ws = self.scratch.get("cand", L.size("sbo_cand_workspace_bytes"))
+                self._call("sbo_cand_sort", self.flags.data_ptr(), self.cand.data_ptr(),
+                           self.nflag.data_ptr(), self.m, self.flags_sorted.data_ptr(),
+                           self.cand_sorted.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
+                self._call("sbo_energy_recheck_cand", self.sig.y.data_ptr(), self.sig.code,
+                           self.m, self.p, self.blocks.data_ptr(), b1, self.s0, self.kind,
+                           self.flags_sorted.data_ptr(), self.cand_sorted.data_ptr(),
+                           self.nflag.data_ptr(), self.m, s.best.data_ptr(),
+                           s.score.data_ptr(), s.residual.data_ptr(), self.stream)
+            else:
+                # incremental (accumulate): only the appended blocks are re-decided,
+                # against the exact score / residual the previous full pass stored
+                incr = accumulate and self.exact_scores
+                self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
+                           self.p, self.blocks.data_ptr(), b0 if incr else 0, b1,
+                           self.s0, self.kind, self.flags.data_ptr(), self.nflag.data_ptr(),
+                           self.m, s.best.data_ptr(), s.score.data_ptr(),
+                           s.residual.data_ptr(), self.stream)
+            self.flag_counts = self.flag_counts[-7:] + [self.nflag.clone()]
+            self.exact_scores = False
             return
         self._call("sbo_energy_pass", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
                    self.blocks.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
@@ -458,6 +485,7 @@ class Engine:
                 ld = max(self.m, 1)
                 self.code(g.perm, g, -1, True, ld, None, None, self.state.score,
                           self.state.residual)
+        self.exact_scores = True
         self.residual()
 
     def rmse(self) -> float:

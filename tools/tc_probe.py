@@ -64,7 +64,7 @@ def main():
         L.call("sbo_tc_energy", tc.yh.data_ptr(), tc.yl.data_ptr(), tc.escale.data_ptr(), tc.m,
                tc.qh.data_ptr(), tc.ql.data_ptr(), tc.fscale.data_ptr(), 0, a.K, a.s0, tc.kind,
                0, s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
-               tc.flags.data_ptr(), tc.nflag.data_ptr(), tc.stream)
+               tc.flags.data_ptr(), tc.nflag.data_ptr(), None, tc.stream)
     t_kernel = timed(only_tc)
     tc.energy(0, a.K, False)
     b_ref, b_tc = ref.state.best.cpu().numpy(), tc.state.best.cpu().numpy()
