@@ -63,6 +63,11 @@ class TorchComm(Comm):
         self.rank = dist.get_rank(group)
 
     def allreduce(self, t):
+        if t.is_cuda and self.dist.get_backend(self.group) != "nccl":
+            h = t.cpu()  # gloo (tests, single-GPU multi-rank runs): through the host
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, group=self.group)
         return t
 
