@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--m", type=int, default=1 << 20, help="signals per GPU")
+    ap.add_argument("--m-per-gpu", dest="m", type=int, default=1 << 20, help="signals per GPU")
     ap.add_argument("--p-edge", type=int, default=8)
     ap.add_argument("--K", type=int, default=16)
     ap.add_argument("--s0", type=int, default=8)
@@ -269,6 +269,17 @@ KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2}
 
 
+def max_over_ranks(x: float, dist, dev) -> float:
+    """Max of a per-rank time over all ranks (NCCL on the device, gloo on the host)."""
+    import torch
+    if dist is None:
+        return x
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -279,11 +290,19 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SBO_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo — a functional check of the
+    # multi-rank path when the box has one GPU (not a performance configuration)
+    one_gpu = os.environ.get("SBO_BENCH_ONE_GPU", "0") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = require_device(local)
     comm = Comm()
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         comm = TorchComm()
     rows, m_total = shard_signals(a, rank, world)
     p = rows.shape[1]
@@ -360,17 +379,15 @@ def run_ours(a):
         marks.append(mk)
     torch.cuda.synchronize()
     elapsed = t_start.elapsed_time(t_end) / 1e3
-    el = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    elapsed = float(el.item())
+    elapsed = max_over_ranks(elapsed, dist if world > 1 else None, dev)
     t_step = elapsed / a.steps
     value = m_total / t_step
     launches = sum(KERNELS_PER_CALL.get(n, 1) * c for n, c in calls.items())
     hbm, bf16, src = peaks()
     kernels = kernel_families(eng.timer, p, min(a.s0, p))
     eng.timer = None
-    dom = max(kernels.items(), key=lambda kv: kv[1]["ms_total"])
+    dom = max(((k, v) for k, v in kernels.items() if v["tflops"]) or kernels.items(),
+              key=lambda kv: kv[1]["ms_total"])
     for v in kernels.values():
         v["ms_per_step"] = v["ms_total"] / a.steps
     f_sig, b_sig = iteration_model(p, a.K, a.s0, a.rounds, 1.0 / 16)
@@ -462,12 +479,9 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
         step()
     e.record()
     torch.cuda.synchronize()
-    t = torch.tensor([s.elapsed_time(e) / 1e3 / a.steps], dtype=torch.float64,
-                     device=eng.dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = max_over_ranks(s.elapsed_time(e) / 1e3 / a.steps, dist, eng.dev)
     m_total = eng.m_total
-    return {"value": m_total / float(t.item()), "unit": "signals/s", "h2d_bytes_per_step": h2d,
+    return {"value": m_total / t, "unit": "signals/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h}
 
 
