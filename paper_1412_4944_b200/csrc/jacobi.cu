@@ -419,7 +419,7 @@ __device__ __forceinline__ void cluster_barrier() {
 // that a single cp.async.bulk shared::cta -> shared::cluster copy delivers to a
 // peer (completing on the peer's mbarrier).  The slice's padding column 16 of
 // row 0 carries the CTA's deviation partial.
-constexpr int kNsSliceLd = 20;
+constexpr int kNsSliceLd = 64 / kNsCluster + 4;  // slice columns + 4: conflict-free fragments
 constexpr int kNsSlice = 64 * kNsSliceLd;  // doubles per slice
 
 __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, uint32_t bytes,
@@ -434,7 +434,8 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
     k_polar_ns_cluster(const double* __restrict__ P, const int64_t* __restrict__ counts,
                        double* Q, int32_t* status) {
   constexpr int N = 64, NC = kNsCluster, W = N / NC, SL = kNsSliceLd, SZ = kNsSlice;
-  static_assert(W == 16, "the fragment mapping below assumes 16-column slices");
+  constexpr int A2 = W / 8;  // 8-column tiles per slice
+  static_assert(W % 8 == 0 && (SL % 16 == 4 || SL % 16 == 12), "slice layout");
   const int r = static_cast<int>(blockIdx.x % NC);  // == %cluster_ctarank for 1-D clusters
   const int b = blockIdx.x / NC;
   __shared__ double red[32];
@@ -480,21 +481,23 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
   bool done = false;
   for (; it < kNsMaxIter; ++it) {
     const double* Xr = X0 + (cur * NC + r) * SZ;                    // this CTA's slice
-    const double* Xw = X0 + (cur * NC + warp / 2) * SZ + 8 * (warp & 1);  // columns 8 warp ..
+    const double* Xw = X0 + (cur * NC + (8 * warp) / W) * SZ + (8 * warp) % W;  // columns 8 warp ..
     // G[16r + 8a + g][8 warp + 2 t4 + h] = sum_k X[k][16r + 8a + g] X[k][8 warp + 2 t4 + h]
-    double gg[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double gg[A2][2];
+#pragma unroll
+    for (int a2 = 0; a2 < A2; ++a2) gg[a2][0] = gg[a2][1] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < N; k0 += 4) {
       const double bv = Xw[(k0 + t4) * SL + g];
 #pragma unroll
-      for (int a2 = 0; a2 < 2; ++a2) dmma64(gg[a2][0], gg[a2][1], Xr[(k0 + t4) * SL + 8 * a2 + g], bv);
+      for (int a2 = 0; a2 < A2; ++a2) dmma64(gg[a2][0], gg[a2][1], Xr[(k0 + t4) * SL + 8 * a2 + g], bv);
     }
     const int gj = 8 * warp + 2 * t4;
     double dsum = 0.0;
     const double al = l < 0.99 ? sqrt(3.0 / (1.0 + l + l * l)) : 1.0;
     const double c1 = 1.5 * al, c3 = -0.5 * al * al * al;
 #pragma unroll
-    for (int a2 = 0; a2 < 2; ++a2) {
+    for (int a2 = 0; a2 < A2; ++a2) {
       const int gi = W * r + 8 * a2 + g;
       const double d0 = gg[a2][0] - (gi == gj ? 1.0 : 0.0);
       const double d1 = gg[a2][1] - (gi == gj + 1 ? 1.0 : 0.0);
@@ -506,18 +509,20 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
     const double part = block_sum<kJacobiThreads>(dsum, red);  // (syncs: As complete)
     l = fmin(1.0, al * l * (3.0 - al * al * l * l) * 0.5);
     // X'[8 warp + g][16r + 8a + 2 t4 + h] = sum_j X[8 warp + g][j] A[j][16r + 8a + 2 t4 + h]
-    double yy[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double yy[A2][2];
+#pragma unroll
+    for (int a2 = 0; a2 < A2; ++a2) yy[a2][0] = yy[a2][1] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < N; k0 += 4) {
       const double av = *at(cur, 8 * warp + g, k0 + t4);
 #pragma unroll
-      for (int a2 = 0; a2 < 2; ++a2)
+      for (int a2 = 0; a2 < A2; ++a2)
         dmma64(yy[a2][0], yy[a2][1], av, As[(k0 + t4) * AL + 8 * a2 + g]);
     }
     const int nxt = cur ^ 1;
     double* mine = X0 + (nxt * NC + r) * SZ;
 #pragma unroll
-    for (int a2 = 0; a2 < 2; ++a2)
+    for (int a2 = 0; a2 < A2; ++a2)
       *reinterpret_cast<double2*>(mine + (8 * warp + g) * SL + 8 * a2 + 2 * t4) =
           make_double2(yy[a2][0], yy[a2][1]);
     if (tid == 0) mine[W] = part;
