@@ -15,6 +15,15 @@ constexpr int kTile = 64;       // signals per CTA tile of the float64 kernels
 constexpr int kThreads = 256;   // threads per CTA of the float64 tile kernels
 
 void set_error(const std::string& msg);
+
+}  // namespace sbo
+
+// round64.cu: Gram partials of a member list on DMMA (p <= 64)
+int sbo_gram_partials64(const void* y, int dtype, int p, const int32_t* members,
+                        const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
+                        int64_t max_seg, double* partial, void* stream);
+
+namespace sbo {
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
 

@@ -77,7 +77,12 @@ __device__ __forceinline__ float select_f(bool c, float a, float b) {
 
 __device__ __forceinline__ int atom_of(int u, int t4) { return 8 * (u >> 1) + 2 * t4 + (u & 1); }
 
-template <typename TY, bool kResid>
+// MODE_ROUND: coding + P partials; MODE_RESID: coding + squared residuals and
+// scores; MODE_GRAM: P partials with X = Y (the Gram matrix of a member list,
+// onb.py:79-95 via thin_svd(ysub) — no block, no coding)
+constexpr int MODE_ROUND = 0, MODE_RESID = 1, MODE_GRAM = 2;
+
+template <typename TY, int MODE>
 __global__ void __launch_bounds__(kThreads, 2) k_round64(
     const TY* __restrict__ y, int p, const int32_t* __restrict__ order,
     const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
@@ -85,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     const double* __restrict__ blocks, int block_override, int k, double* partial,
     double* rest_sq, int kind, double* score) {
   constexpr int NB = Stage<TY>::NB, YLD = Stage<TY>::YLD;
+  constexpr bool kResid = MODE == MODE_RESID;
   if (static_cast<int>(blockIdx.x) >= *nseg) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const Layout<TY> L;
@@ -97,12 +103,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
   double* scr = reinterpret_cast<double*>(smem + L.scr_off) + warp * 64;
   unsigned char* fl = smem + L.flag_off + warp * 64;
   const int seg = blockIdx.x;
-  const int b = block_override >= 0 ? block_override : seg_block[seg];
   const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
-  const double* q = blocks + static_cast<int64_t>(b) * p * p;
-  for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
-    const int kk = e >> 6, ii = e & 63;
-    sQ[kk * LD + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+  if constexpr (MODE != MODE_GRAM) {
+    const int b = block_override >= 0 ? block_override : seg_block[seg];
+    const double* q = blocks + static_cast<int64_t>(b) * p * p;
+    for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
+      const int kk = e >> 6, ii = e & 63;
+      sQ[kk * LD + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+    }
   }
   // P accumulator (outer mode), DMMA fragments: warp w owns rows [8w, 8w+8) x 64 atoms
   double acc[8][2];
@@ -151,9 +159,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     if (NB == 2 && t0 + kTile < hi) stage(t0 + kTile, buf ^ 1);  // in flight during this tile
     const TY* sY = sYall + buf * kTile * YLD;
     const int64_t* rows = rowsall + buf * kTile;
+    const int s = 8 * warp + g;
+    if constexpr (MODE == MODE_GRAM) {
+      // X = Y (zero rows for inactive signals are already zero in sY)
+      double* xr = X + s * LD + 2 * t4;
+      const TY* yr = sY + s * YLD + 2 * t4;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+        *reinterpret_cast<double2*>(xr + 8 * n) =
+            make_double2(static_cast<double>(yr[8 * n]), static_cast<double>(yr[8 * n + 1]));
+    } else {
     // C = Y_tile . Q: this quad's signal s = 8 warp + g, coefficients c[n][h] of
     // atoms 8n + 2 t4 + h
-    const int s = 8 * warp + g;
     double c[8][2];
 #pragma unroll
     for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
@@ -249,6 +266,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
         *reinterpret_cast<double2*>(xr + 8 * n) =
             make_double2(((mask >> (2 * n)) & 1u) ? c[n][0] : 0.0,
                          ((mask >> (2 * n + 1)) & 1u) ? c[n][1] : 0.0);
+    }
+    }  // MODE != MODE_GRAM
+    if constexpr (!kResid) {
       __syncthreads();
       // P[kk][i] += sum_s Y[s][kk] X[s][i] on DMMA, signals in order (inactive
       // rows are zero in both Y and X)
@@ -275,18 +295,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
   }
 }
 
-template <typename TY, bool kResid>
+template <typename TY, int MODE>
 int launch(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
            const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
            const double* blocks, int block_override, int k, double* partial, double* rest_sq,
            int kind, double* score, cudaStream_t st) {
   const Layout<TY> L;
-  cudaFuncSetAttribute(k_round64<TY, kResid>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_round64<TY, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
-  k_round64<TY, kResid><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
+  k_round64<TY, MODE><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
       block_override, k, partial, rest_sq, kind, score);
-  return check_launch(kResid ? "k_round64<resid>" : "k_round64");
+  return check_launch(MODE == MODE_RESID ? "k_round64<resid>"
+                                         : (MODE == MODE_GRAM ? "k_round64<gram>" : "k_round64"));
 }
 
 int check(int dtype, int p, int s0) {
@@ -311,10 +332,10 @@ extern "C" int sbo_round_segments(const void* y, int dtype, int p, const int32_t
   if (max_seg <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32
-             ? r64::launch<float, false>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+             ? r64::launch<float, r64::MODE_ROUND>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
                                          blocks, block_override, k, partial, nullptr,
                                          SBO_KIND_SQUARED_SUM, nullptr, as_stream(stream))
-             : r64::launch<double, false>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+             : r64::launch<double, r64::MODE_ROUND>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
                                           blocks, block_override, k, partial, nullptr,
                                           SBO_KIND_SQUARED_SUM, nullptr, as_stream(stream));
 }
@@ -330,10 +351,27 @@ extern "C" int sbo_residual_segments(const void* y, int dtype, int p, const int3
   if (max_seg <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32
-             ? r64::launch<float, true>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+             ? r64::launch<float, r64::MODE_RESID>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
                                         blocks, -1, k, nullptr, rest_sq, kind, score,
                                         as_stream(stream))
-             : r64::launch<double, true>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
+             : r64::launch<double, r64::MODE_RESID>(y, p, order, seg_block, seg_lo, seg_hi, nseg, max_seg,
                                          blocks, -1, k, nullptr, rest_sq, kind, score,
                                          as_stream(stream));
+}
+
+// Gram partials of a member list for p <= 64 on DMMA (used by sbo_gram): one
+// p x p partial per segment of the list, in member order.
+int sbo_gram_partials64(const void* y, int dtype, int p, const int32_t* members,
+                        const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
+                        int64_t max_seg, double* partial, void* stream) {
+  if (max_seg <= 0) return SBO_OK;
+  return dtype == SBO_F32
+             ? r64::launch<float, r64::MODE_GRAM>(y, p, members, nullptr, seg_lo, seg_hi, nseg,
+                                                  max_seg, nullptr, 0, 1, partial, nullptr,
+                                                  SBO_KIND_SQUARED_SUM, nullptr,
+                                                  as_stream(stream))
+             : r64::launch<double, r64::MODE_GRAM>(y, p, members, nullptr, seg_lo, seg_hi,
+                                                   nseg, max_seg, nullptr, 0, 1, partial,
+                                                   nullptr, SBO_KIND_SQUARED_SUM, nullptr,
+                                                   as_stream(stream));
 }

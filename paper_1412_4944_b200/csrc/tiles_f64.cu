@@ -756,10 +756,11 @@ extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members,
   int64_t* hi = lo + n;
   int32_t* ns = reinterpret_cast<int32_t*>(hi + n);
   k_chunk_segments<<<1, 256, 0, st>>>(w, chunk, lo, hi, ns);
-  int rc = dtype == SBO_F32 ? outer_impl<float>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
-                                                nullptr, 1, partial, st)
-                            : outer_impl<double>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
-                                                 nullptr, 1, partial, st);
+  int rc = p <= 64 ? sbo_gram_partials64(y, dtype, p, members, lo, hi, ns, n, partial, st)
+           : dtype == SBO_F32 ? outer_impl<float>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
+                                                  nullptr, 1, partial, st)
+                              : outer_impl<double>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
+                                                   nullptr, 1, partial, st);
   if (rc) return rc;
   const int64_t pp = static_cast<int64_t>(p) * p;
   k_reduce_segments<<<dim3(static_cast<unsigned>(ceil_div(pp, 32)), 1), 256, 0, st>>>(
