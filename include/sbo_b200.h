@@ -169,7 +169,7 @@ int sbo_outer_segments(const void* y, int dtype, int p, const int32_t* order, co
 int sbo_reduce_segments(const double* partial, const int32_t* seg_block, const int32_t* nseg,
                         int64_t max_seg, int K, int p, double* P, void* stream);
 
-/* Fused 1ONB round for p <= 64 and min(s0, p) < 16 — onb.py:170-171 (coding of
+/* Fused 1ONB round for p <= 64, any s0 — onb.py:170-171 (coding of
  * every signal in its own block, then P = Y X^T) in one pass per segment: the
  * same partials as sbo_code_segments + sbo_outer_segments, codes not stored. */
 int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
@@ -177,7 +177,7 @@ int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
                        const int32_t* nseg, int64_t max_seg, const double* blocks,
                        int block_override, int s0, double* partial, void* stream);
 
-/* Squared residuals of represent (sbo.py:213-218) for p <= 64, min(s0, p) < 16:
+/* Squared residuals of represent (sbo.py:213-218) for p <= 64, any s0:
  * every signal of a segment is coded in its segment's block in float64 (exact
  * selection, as sbo_code_segments) and rest_sq[order[t]] receives the energy of
  * its discarded coefficients; score (optional) the exact energy of the kind

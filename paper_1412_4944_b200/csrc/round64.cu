@@ -1,4 +1,4 @@
-// The 1ONB round for p <= 64, min(s0, p) < 16 (onb.py:170-171), fused per block
+// The 1ONB round for p <= 64 (onb.py:170-171), any s0, fused per block
 // segment: float64 projection on the DMMA tensor cores, exact top-k selection
 // in registers, and the sparse outer product P += Y X^T in signal order.
 //
@@ -11,7 +11,7 @@
 //   magnitudes differ the kept set is exactly {i : fp32|c_i| >= t_k} — the
 //   float64 stable-argsort set.  A quad bitonic network finds t_k; a signal
 //   whose fp32 k-th/(k+1)-th magnitudes tie is re-decided by its warp with the
-//   exact rank rule (pick_row).
+//   exact rank rule (pick_row).  For k >= 16 every signal takes that path.
 // * Outer product (sparse_outer, onb.py:127-134): the kept values are written as
 //   a dense X tile (zeros elsewhere) and P += Y^T X runs on DMMA in signal order
 //   (deterministic partials, no atomics).  A sparse DFMA form (2 p k flop per
@@ -27,7 +27,6 @@ namespace sbo {
 namespace r64 {
 
 constexpr int LD = 68;  // float64 row stride of the block / X tiles (conflict-free fragments)
-constexpr int KMAX = 16;
 
 // Signal tiles are staged in their storage type: float32 rows (stride 72 floats,
 // conflict-free DMMA fragment loads, double-buffered: the next tile's cp.async
@@ -190,31 +189,69 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     auto mag = [&](int u) -> float {
       return (act && atom_of(u, t4) < p) ? static_cast<float>(fabs(c[u >> 1][u & 1])) : -1.0f;
     };
-    float srt[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) srt[u] = mag(u);
-    topk::sort_desc<16>(srt);
-#pragma unroll
-    for (int x = 1; x <= 2; x <<= 1) {
-      float other[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) other[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
-      topk::merge_top<16>(srt, other);
-    }
-    // the k-th / (k+1)-th largest by register selects (a plain srt[k - 1] with
-    // runtime k would go through local memory)
-    float tk = srt[0], tk1 = srt[1];
-#pragma unroll
-    for (int u = 1; u < 16; ++u) {
-      tk = select_f(u == k - 1, srt[u], tk);
-      tk1 = select_f(u == k, srt[u], tk1);
-    }
     uint32_t mask = 0u;
+    unsigned need;
+    if (k < 16) {
+      float srt[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u)
-      if (mag(u) >= tk && mag(u) >= 0.0f) mask |= 1u << u;
-    // float32 ties at the threshold: the warp re-decides those signals exactly
-    unsigned need = __ballot_sync(0xffffffffu, act && !(tk > tk1) && t4 == 0);
+      for (int u = 0; u < 16; ++u) srt[u] = mag(u);
+      topk::sort_desc<16>(srt);
+#pragma unroll
+      for (int x = 1; x <= 2; x <<= 1) {
+        float other[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) other[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
+        topk::merge_top<16>(srt, other);
+      }
+      // the k-th / (k+1)-th largest by register selects (a plain srt[k - 1] with
+      // runtime k would go through local memory)
+      float tk = srt[0], tk1 = srt[1];
+#pragma unroll
+      for (int u = 1; u < 16; ++u) {
+        tk = select_f(u == k - 1, srt[u], tk);
+        tk1 = select_f(u == k, srt[u], tk1);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (mag(u) >= tk && mag(u) >= 0.0f) mask |= 1u << u;
+      // float32 ties at the threshold: the warp re-decides those signals exactly
+      need = __ballot_sync(0xffffffffu, act && !(tk > tk1) && t4 == 0);
+    } else {
+      // k >= 16: the k-th largest fp32 magnitude of the quad's 64 by bisection on
+      // its bit pattern (non-negative floats order like their bits): the largest T
+      // with #{|c| >= T} >= k.  Exactly k at or above T: the kept set; otherwise a
+      // tie at the threshold, re-decided by the warp's exact rank rule.
+      uint32_t key[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) key[u] = mag(u) >= 0.0f ? __float_as_uint(mag(u)) : 0u;
+      const uint32_t vmask = [&] {
+        uint32_t v = 0u;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v |= (act && atom_of(u, t4) < p ? 1u : 0u) << u;
+        return v;
+      }();
+      uint32_t T = 0u;
+#pragma unroll 1
+      for (int bit = 30; bit >= 0; --bit) {
+        const uint32_t cand = T | (1u << bit);
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) cnt += ((vmask >> u) & 1u) && key[u] >= cand;
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+        if (cnt >= k) T = cand;
+      }
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const bool on = ((vmask >> u) & 1u) && key[u] >= T;
+        cnt += on;
+        if (on) mask |= 1u << u;
+      }
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+      need = __ballot_sync(0xffffffffu, act && cnt != k && t4 == 0);
+    }
     double rest = -1.0, fscore = 0.0;  // rest < 0: not decided by the fallback
     while (need) {
       const int gg = (__ffs(need) - 1) >> 2;
@@ -314,7 +351,7 @@ int check(int dtype, int p, int s0) {
   if (dtype != SBO_F32 && dtype != SBO_F64) return fail(SBO_EINVAL, "bad dtype");
   if (p < 1 || p > 64) return fail(SBO_EINVAL, "the fused round needs p <= 64");
   const int k = s0 < p ? s0 : p;
-  if (s0 < 1 || k >= KMAX) return fail(SBO_EINVAL, "the fused round needs 1 <= min(s0, p) < 16");
+  if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
   return SBO_OK;
 }
 

@@ -404,7 +404,7 @@ class Engine:
         val = self.scratch.get("tr_val", 8 * self.k * ld).view(torch.float64)
         pol_ws = self.scratch.get("polar", L.size("sbo_polar_workspace_bytes", nblocks, p))
         Pt = P[: 8 * nblocks * p * p].view(torch.float64).view(nblocks, p, p)
-        fused = p <= 64 and self.k < 16 and os.environ.get("SBO_FUSED_ROUND", "1") != "0"
+        fused = p <= 64 and os.environ.get("SBO_FUSED_ROUND", "1") != "0"
         override = first_block if single else -1
         for r in range(rounds):
             if fused:  # coding + P partials in one pass per segment
@@ -479,7 +479,7 @@ class Engine:
             # float32-accurate, so recode every signal in its winning block in
             # float64 (exact support + discarded energy), as the worst set needs
             g = self.group(self.K)
-            if self.p <= 64 and self.k < 16:
+            if self.p <= 64:
                 self._call("sbo_residual_segments", self.sig.y.data_ptr(), self.sig.code,
                            self.p, g.perm.data_ptr(), g.seg_block.data_ptr(),
                            g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(),

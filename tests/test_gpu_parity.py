@@ -377,13 +377,14 @@ def test_sbo_train_fixed_point():
     assert d.num_blocks == 1 and rep.rows[-1].rmse <= 1e-8
 
 
-def test_iteration_zero_and_duplicate_signals(dev):
+@pytest.mark.parametrize("s0", [8, 16])
+def test_iteration_zero_and_duplicate_signals(dev, s0):
     """Multi-tile segments mixing all-zero signals (every coefficient ties at 0: the
     exact rank fallback, index order), small duplicated signals (scaled below the
     worst set, which would otherwise be rank-deficient) and Gaussian ones:
     represent, the fused rounds and the residual pass vs the oracle."""
     rng = np.random.default_rng(21)
-    p, m, K, s0 = 64, 24576, 4, 8
+    p, m, K = 64, 24576, 4
     y32 = rng.standard_normal((m, p)).astype(np.float32)
     y32[rng.random(m) < 0.2] = 0.0
     dup = rng.random(m) < 0.2
