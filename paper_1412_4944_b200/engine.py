@@ -438,6 +438,13 @@ class Engine:
 
     def init_block(self, G, ncols: int, draws: np.ndarray, slot: int, status, rank=None):
         self.reset_rotation(slot, slot + 1)
+        if torch.is_tensor(draws) and draws.is_cuda:  # already staged on the device
+            d = draws.to(torch.float64).contiguous()
+            ws = self.scratch.get("init", L.size("sbo_init_workspace_bytes", self.p))
+            self._call("sbo_init_block", G.data_ptr(), self.p, ncols, d.data_ptr(), d.shape[0],
+                       self.block_ptr(slot), _ptr(rank), status.data_ptr(), ws.data_ptr(),
+                       ws.numel(), self.stream)
+            return
         # staged through a persistent pinned buffer and copied asynchronously (a
         # pageable copy would synchronise); the buffer is reused only after the
         # iteration's closing synchronisation

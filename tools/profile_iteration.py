@@ -20,14 +20,16 @@ def main():
     ap.add_argument("--m", type=int, default=1 << 20)
     ap.add_argument("--K", type=int, default=16)
     ap.add_argument("--iters", type=int, default=1)
+    ap.add_argument("--p-edge", type=int, default=8)
+    ap.add_argument("--s0", type=int, default=8)
     a = ap.parse_args()
     dev = require_device()
-    rows = signals.unit_range(signals.patch_bytes(signals.scene(2048, 2048, 0), 8, a.m, 11))
-    eng = Engine(Signals.from_rows(rows, dev), 8, k_cap=a.K)
-    _init_into(eng, SboConfig(s0=8, k0=a.K - 1, p0=4096, rounds=6, k_max=a.K, seed=1), a.m)
+    rows = signals.unit_range(signals.patch_bytes(signals.scene(2048, 2048, 0), a.p_edge, a.m, 11))
+    eng = Engine(Signals.from_rows(rows, dev), a.s0, k_cap=a.K)
+    _init_into(eng, SboConfig(s0=a.s0, k0=a.K - 1, p0=4096, rounds=6, k_max=a.K, seed=1), a.m)
     eng.represent_full()
     torch.cuda.synchronize()
-    draws = _block_rng(1, 1, eng.K).standard_normal((72, 64))
+    draws = _block_rng(1, 1, eng.K).standard_normal((eng.p + 8, eng.p))
     K0 = eng.K
     snap = eng.blocks.clone()
     for _ in range(a.iters):
