@@ -798,8 +798,14 @@ size_t init_smem_bytes(int p) {
 constexpr size_t kSmemBudget = 200 * 1024;
 }  // namespace
 
+extern "C" size_t sbo_polar_ns_big_workspace_bytes(int K, int p);
+int sbo_polar_ns_big(const double* P, int K, int p, const int64_t* counts, double* Q,
+                     int32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 extern "C" size_t sbo_polar_workspace_bytes(int K, int p) {
-  return static_cast<size_t>(K) * polar_smem_bytes(p) + 64;
+  const size_t jac = static_cast<size_t>(K) * polar_smem_bytes(p) + 64;
+  const size_t ns = p > 64 ? sbo_polar_ns_big_workspace_bytes(K, p) : 0;
+  return jac > ns ? jac : ns;
 }
 
 extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, double* Q,
@@ -813,6 +819,10 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
   // p = 64: Newton-Schulz first; Jacobi only for the matrices it hands back
   static const bool force_jacobi = getenv("SBO_POLAR_JACOBI") != nullptr;
   const bool ns = p == 64 && status && !sigma && !force_jacobi;
+  const bool ns_big = p > 64 && status && !sigma && !force_jacobi;
+  if (ns_big) {  // batched DMMA Newton-Schulz; Jacobi below for what it hands back
+    if (int rc = sbo_polar_ns_big(P, K, p, counts, Q, status, ws, ws_bytes, stream)) return rc;
+  }
   if (ns) {
     static const bool single = getenv("SBO_POLAR_SINGLE_CTA") != nullptr;
     if (single) {
@@ -839,7 +849,7 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
         P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), ns ? 1 : 0);
   } else {
     k_polar<false><<<K, kJacobiThreads, 0, as_stream(stream)>>>(
-        P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), 0);
+        P, p, counts, Q, V, sigma, status, static_cast<double*>(ws), ns_big ? 1 : 0);
   }
   return check_launch("k_polar");
 }
