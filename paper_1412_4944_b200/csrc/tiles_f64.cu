@@ -78,52 +78,45 @@ __device__ void project64_dmma(const double* sY, const double* sQ, double* C) {
     *reinterpret_cast<double2*>(crow + 8 * n) = make_double2(c[n][0], c[n][1]);
 }
 
-// C[s][i] = sum_k y[rows[s]][k] * Q[k][i]  (float64 FMA chain over k ascending)
+// p > 64: C[s][i] = sum_k y[rows[s]][k] Q[k][i] on DMMA in 64 x 64 chunks — per
+// 64-atom column chunk, the 64-wide K chunks are staged (sY[s][k], sQ[k][i], row
+// stride 68) and accumulated in the warps' fragments (warp w: signals 8w..8w+8).
 template <typename TY>
-__device__ void project_tile(const TY* __restrict__ y, int p, const int64_t* rows,
-                             const double* __restrict__ q, double* C, int ldc, double* sY,
-                             double* sQ) {
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+__device__ void project_tile_dmma(const TY* __restrict__ y, int p, const int64_t* rows,
+                                  const double* __restrict__ q, double* C, int ldc, double* sY,
+                                  double* sQ) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   for (int ic = 0; ic < p; ic += 64) {
-    const int in = min(64, p - ic);
-    double acc[4][4];
+    double c[8][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
     for (int kc = 0; kc < p; kc += 64) {
-      const int kn = min(64, p - kc);
       __syncthreads();
       for (int e = tid; e < kTile * 64; e += kThreads) {
         const int s = e >> 6, kk = e & 63;
         const int64_t r = rows[s];
-        double v = 0.0;
-        if (r >= 0 && kk < kn) v = static_cast<double>(__ldg(y + r * p + kc + kk));
-        sY[kk * kSyLd + s] = v;
-      }
-      for (int e = tid; e < 64 * 64; e += kThreads) {
-        const int kk = e >> 6, ii = e & 63;
-        sQ[e] = (kk < kn && ii < in) ? __ldg(q + static_cast<int64_t>(kc + kk) * p + ic + ii) : 0.0;
+        sY[s * kDmmaLd + kk] =
+            (r >= 0 && kc + kk < p) ? static_cast<double>(__ldg(y + r * p + kc + kk)) : 0.0;
+        sQ[s * kDmmaLd + kk] = (kc + s < p && ic + kk < p)
+                                   ? __ldg(q + static_cast<int64_t>(kc + s) * p + ic + kk)
+                                   : 0.0;
       }
       __syncthreads();
-      for (int kk = 0; kk < kn; ++kk) {
-        const double2 y01 = *reinterpret_cast<const double2*>(sY + kk * kSyLd + 4 * ty);
-        const double2 y23 = *reinterpret_cast<const double2*>(sY + kk * kSyLd + 4 * ty + 2);
-        const double2 q01 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx);
-        const double2 q23 = *reinterpret_cast<const double2*>(sQ + kk * 64 + 4 * tx + 2);
-        const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
-        const double qv[4] = {q01.x, q01.y, q23.x, q23.y};
+      const double* ya = sY + (8 * warp + g) * kDmmaLd + t4;
+#pragma unroll 4
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const double a = ya[k0];
+        const double* qb = sQ + (k0 + t4) * kDmmaLd + g;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(yv[a], qv[b], acc[a][b]);
+        for (int n = 0; n < 8; ++n) dmma8(c[n][0], c[n][1], a, qb[8 * n]);
       }
     }
+    double* crow = C + (8 * warp + g) * ldc + ic + 2 * t4;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int n = 0; n < 8; ++n)
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (4 * tx + b < in) C[(4 * ty + a) * ldc + ic + 4 * tx + b] = acc[a][b];
+      for (int h = 0; h < 2; ++h)
+        if (ic + 8 * n + 2 * t4 + h < p) crow[8 * n + h] = c[n][h];
   }
   __syncthreads();
 }
@@ -263,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
         project64_dmma(sY, sQ, C);
         __syncthreads();
       } else {
-        project_tile(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
+        project_tile_dmma(y, p, rows, blocks + static_cast<int64_t>(b) * p * p, C, L.ldc, sY, sQ);
       }
       if (p <= 64 && k < 16) {
         const int s = threadIdx.x >> 2;
@@ -351,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_code_f64(
       project64_dmma(sY, sQ, C);
       __syncthreads();
     } else {
-      project_tile(y, p, rows, q, C, L.ldc, sY, sQ);
+      project_tile_dmma(y, p, rows, q, C, L.ldc, sY, sQ);
     }
     int* fb = reinterpret_cast<int*>(smem + L.misc_off);
     const bool quad = p <= 64 && k < 16;
