@@ -17,6 +17,8 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -677,11 +679,94 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
   }
 }
 
+// A = G (col-major), V = I: the Jacobi starting point (one CTA per column)
+__global__ void k_fill_gram(const double* __restrict__ G, int p, double* A, double* V) {
+  const int c = blockIdx.x;
+  for (int r = threadIdx.x; r < p; r += blockDim.x) {
+    A[static_cast<int64_t>(c) * p + r] = G[static_cast<int64_t>(r) * p + c];
+    V[static_cast<int64_t>(c) * p + r] = r == c ? 1.0 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One-sided Jacobi for 64 < p <= 256 over the whole GPU: a cooperative grid whose
+// warps take the p/2 column pairs of each tournament step (columns in global
+// memory, L2-resident), with a grid-wide barrier between steps.  Same rotations,
+// tolerances and ordering as jacobi_sweeps; A = G, V = I on entry (col-major).
+// The sweep count (or -1) is written to *sweeps_out.
+__global__ void __launch_bounds__(256) k_jacobi_grid(double* A, double* V, int rows, int p,
+                                                     int* flag, int* sweeps_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int wg = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int nw = static_cast<int>(gridDim.x) * 8;
+  const int n = p + (p & 1), npairs = n >> 1;
+  const double tol = jacobi_rot_tol(), conv = jacobi_conv_tol(rows);
+  int result = -1;
+  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    if (grid.thread_rank() == 0) *flag = 0;
+    grid.sync();
+    for (int step = 0; step < n - 1; ++step) {
+      for (int q = wg; q < npairs; q += nw) {
+        int i, j;
+        if (q == 0) {
+          i = step;
+          j = n - 1;
+        } else {
+          i = (step + q) % (n - 1);
+          j = (step - q + n - 1) % (n - 1);
+        }
+        if (i >= p || j >= p) continue;
+        double* ai = A + static_cast<int64_t>(i) * rows;
+        double* aj = A + static_cast<int64_t>(j) * rows;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < rows; r += 32) {
+          const double x = ai[r], y = aj[r];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        const double g2 = ga * ga, ab = al * be;
+        if (al > 0.0 && be > 0.0 && g2 > tol * tol * ab) {
+          double c, sn;
+          rotation(al, be, ga, c, sn);
+          for (int r = lane; r < rows; r += 32) {
+            const double x = ai[r], y = aj[r];
+            ai[r] = c * x - sn * y;
+            aj[r] = sn * x + c * y;
+          }
+          double* vi = V + static_cast<int64_t>(i) * p;
+          double* vj = V + static_cast<int64_t>(j) * p;
+          for (int r = lane; r < p; r += 32) {
+            const double x = vi[r], y = vj[r];
+            vi[r] = c * x - sn * y;
+            vj[r] = sn * x + c * y;
+          }
+          if (lane == 0 && g2 > conv * conv * ab) atomicExch(flag, 1);
+        }
+      }
+      grid.sync();
+    }
+    const int moving = *reinterpret_cast<volatile int*>(flag);
+    grid.sync();  // everyone has read the flag before it is reset
+    if (!moving) {
+      result = sweep + 1;
+      break;
+    }
+  }
+  if (grid.thread_rank() == 0) *sweeps_out = result;
+}
+
 // ---------------------------------------------------------------------------
 template <bool SMEM, int NT>
 __global__ void __launch_bounds__(NT) k_init_block(
     const double* __restrict__ G, int p, int64_t ncols, const double* __restrict__ draws,
-    int ndraws, double* Q, int32_t* rank_out, int32_t* status, double* ws, int use_smem) {
+    int ndraws, double* Q, int32_t* rank_out, int32_t* status, double* ws, int use_smem,
+    const int* presolved_sweeps = nullptr) {
   const int64_t pp = static_cast<int64_t>(p) * p;
   __shared__ JacobiSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -695,13 +780,18 @@ __global__ void __launch_bounds__(NT) k_init_block(
   U = V + pp;
   lam = U + pp;
   ord = reinterpret_cast<int*>(lam + p);
-  for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
-    const int r = static_cast<int>(e / p), c = static_cast<int>(e % p);
-    A[static_cast<int64_t>(c) * p + r] = G[e];
-    V[static_cast<int64_t>(c) * p + r] = (r == c) ? 1.0 : 0.0;
+  int sweeps;
+  if (presolved_sweeps) {  // A, V already rotated by k_jacobi_grid
+    sweeps = *presolved_sweeps;
+  } else {
+    for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
+      const int r = static_cast<int>(e / p), c = static_cast<int>(e % p);
+      A[static_cast<int64_t>(c) * p + r] = G[e];
+      V[static_cast<int64_t>(c) * p + r] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    sweeps = jacobi_sweeps(A, V, p, p, &S.flag);
   }
-  __syncthreads();
-  const int sweeps = jacobi_sweeps(A, V, p, p, &S.flag);
   column_order(A, p, p, lam, ord, true);  // |G v_j| = lambda_j
   const double l0 = lam[ord[0]];
   // kept directions: sqrt(l) > 1e-12 sqrt(l0) and above the Gram floor; at most ncols
@@ -854,7 +944,7 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
   return check_launch("k_polar");
 }
 
-extern "C" size_t sbo_init_workspace_bytes(int p) { return init_smem_bytes(p) + 64; }
+extern "C" size_t sbo_init_workspace_bytes(int p) { return init_smem_bytes(p) + 64; }  // + 2 ints
 
 extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const double* draws,
                               int ndraws, double* Q, int32_t* rank, int32_t* status, void* ws,
@@ -877,8 +967,23 @@ extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const doubl
           G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
     }
   } else {
+    // large p: the sweeps on a cooperative grid, then the single-CTA finish
+    double* A = static_cast<double*>(ws);
+    double* V = A + static_cast<int64_t>(p) * p;
+    int* aux = reinterpret_cast<int*>(static_cast<char*>(ws) + init_smem_bytes(p));
+    k_fill_gram<<<p, 256, 0, as_stream(stream)>>>(G, p, A, V);
+    int* flag = aux;
+    int* sweeps = aux + 1;
+    int rows = p, pp_ = p;
+    void* args[] = {&A, &V, &rows, &pp_, &flag, &sweeps};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = (p / 2 + 7) / 8 < sms ? (p / 2 + 7) / 8 : sms;
+    SBO_CHECK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_jacobi_grid), blocks,
+                                               256, args, 0, as_stream(stream)));
     k_init_block<false, kJacobiThreads><<<1, kJacobiThreads, 0, as_stream(stream)>>>(
-        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 0);
+        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 0, sweeps);
   }
   return check_launch("k_init_block");
 }
