@@ -52,7 +52,7 @@ def parse():
 
 def workload_name(a, world):
     return (f"B: p={a.p_edge**2}, K={a.K} (entering {a.K - 1}), s0={a.s0}, R={a.rounds}, "
-            f"m=2^{int(math.log2(a.m))} per GPU x {world}, W=m/16, 8x8 patches of a "
+            f"m=2^{int(math.log2(a.m))} per GPU x {world}, W=m/16, {a.p_edge}x{a.p_edge} patches of a "
             f"{a.scene}^2 synthetic scene")
 
 
