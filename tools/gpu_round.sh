@@ -11,5 +11,5 @@ timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/b
 timeout 900 ncu --nvtx --nvtx-include "iteration/" --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file gpurun_out/launches.csv python tools/profile_iteration.py > gpurun_out/launches.log 2>&1
 python tools/launch_summary.py gpurun_out/launches.csv 24 > gpurun_out/launch_summary.txt 2>&1
-NCU_SPECS=${NCU_SPECS:-"round_retrain:k_round64:6 energy16:k_energy_tc:1 resid:k_round64:12 polar:k_polar_ns_cluster:6 init:k_init_block:0"} bash tools/gpu_prof.sh
+NCU_SPECS=${NCU_SPECS:-"round_retrain:k_round64:7 energy16:k_energy_tc:1 resid:k_round64:13 polar:k_polar_ns_cluster:6 init:k_init_block:0"} bash tools/gpu_prof.sh
 tail -5 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/smoke.log; tail -c 600 gpurun_out/bench.log; cat gpurun_out/launch_summary.txt
