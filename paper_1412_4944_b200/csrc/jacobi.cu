@@ -107,20 +107,25 @@ __device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) 
         if (al[h] > 0.0 && be[h] > 0.0 && g2 > tol2 * ab) {
           double c, sn;
           rotation(al[h], be[h], ga[h], c, sn);
-          double* vi = V + (h ? i1 : i0) * N + lg;
-          double* vj = V + (h ? j1 : j0) * N + lg;
-          double vx[4], vy[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            vx[u] = vi[16 * u];
-            vy[u] = vj[16 * u];
-          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             ai[h][16 * u] = c * x[h][u] - sn * y[h][u];
             aj[h][16 * u] = sn * x[h][u] + c * y[h][u];
-            vi[16 * u] = c * vx[u] - sn * vy[u];
-            vj[16 * u] = sn * vx[u] + c * vy[u];
+          }
+          if (V) {  // V == nullptr: only the orthogonalised columns are wanted
+            double* vi = V + (h ? i1 : i0) * N + lg;
+            double* vj = V + (h ? j1 : j0) * N + lg;
+            double vx[4], vy[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              vx[u] = vi[16 * u];
+              vy[u] = vj[16 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              vi[16 * u] = c * vx[u] - sn * vy[u];
+              vj[16 * u] = sn * vx[u] + c * vy[u];
+            }
           }
           if (lg == 0 && g2 > conv2 * ab) *flag = 1;
         }
@@ -679,6 +684,110 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
   }
 }
 
+// Eigenvectors of a 64 x 64 symmetric PSD G (the worst set's Gram matrix) by
+// Drmac-Veselic preconditioning: pivoted Cholesky P^T G P = R^T R (largest
+// remaining diagonal first), then one-sided Jacobi on the columns of X = R^T,
+// which converges in a few sweeps from this start; X V = U Sigma gives
+// R^T R = U Sigma^2 U^T, so G's eigenvectors are P U (rows permuted back) with
+// eigenvalues sigma_j^2.  Columns whose sigma is negligible come out zero (the
+// caller's rank test drops them and completes the basis).  512 threads.
+// Out: V col-major eigenvectors (unordered), lam[j] = sigma_j^2.  Returns sweeps.
+__device__ int init_eig64_precond(const double* __restrict__ G, double* A, double* V,
+                                  double* W, double* lam, int* perm, int* flag) {
+  constexpr int N = 64, LDW = 65;
+  const int tid = threadIdx.x;
+  __shared__ int piv;
+  __shared__ double dmax0;
+  // W = G (row-major, stride 65), perm = identity
+  for (int e = tid; e < N * N; e += 512) W[(e >> 6) * LDW + (e & 63)] = G[e];
+  if (tid < N) perm[tid] = tid;
+  __syncthreads();
+  int rank = N;
+  for (int k = 0; k < N; ++k) {
+    if (tid < 32) {  // pivot: largest remaining diagonal, lowest index on ties
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < N; i += 32) {
+        const double d = W[i * LDW + i];
+        if (d > best) {
+          best = d;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (tid == 0) {
+        piv = bi;
+        if (k == 0) dmax0 = best;
+      }
+    }
+    __syncthreads();
+    const int j = piv;
+    if (j != k) {  // symmetric swap of rows / columns k and j, and of the permutation
+      for (int c = tid; c < N; c += 512) {
+        const double t = W[k * LDW + c];
+        W[k * LDW + c] = W[j * LDW + c];
+        W[j * LDW + c] = t;
+      }
+      __syncthreads();
+      for (int r = tid; r < N; r += 512) {
+        const double t = W[r * LDW + k];
+        W[r * LDW + k] = W[r * LDW + j];
+        W[r * LDW + j] = t;
+      }
+      if (tid == 0) {
+        const int t = perm[k];
+        perm[k] = perm[j];
+        perm[j] = t;
+      }
+      __syncthreads();
+    }
+    const double d = W[k * LDW + k];
+    if (!(d > 64.0 * DBL_EPSILON * dmax0) || !(d > 0.0)) {  // the rest is numerically zero
+      rank = k;
+      break;
+    }
+    const double rkk = sqrt(d);
+    // row k of R: R[k][k] = sqrt(d), R[k][c] = W[k][c] / R[k][k] (c > k)
+    for (int c = tid; c < N; c += 512) W[k * LDW + c] = c < k ? 0.0 : (c == k ? rkk : W[k * LDW + c] / rkk);
+    __syncthreads();
+    // Schur complement of the trailing block
+    for (int e = tid; e < N * N; e += 512) {
+      const int r = e >> 6, c = e & 63;
+      if (r > k && c > k) W[r * LDW + c] = fma(-W[k * LDW + r], W[k * LDW + c], W[r * LDW + c]);
+    }
+    __syncthreads();
+  }
+  // X = R^T as A col-major: column j of A = row j of R (rows >= rank are zero)
+  for (int e = tid; e < N * N; e += 512) {
+    const int j = e >> 6, r = e & 63;
+    A[e] = (j < rank && r >= j) ? W[j * LDW + r] : 0.0;
+  }
+  __syncthreads();
+  const int sweeps = jacobi_sweeps64<512>(A, nullptr, flag);
+  // sigma_j = ||A_j||; eigenvector j of G = P (A_j / sigma_j)
+  if (tid < N) {
+    double ss = 0.0;
+    for (int r = 0; r < N; ++r) ss = fma(A[tid * N + r], A[tid * N + r], ss);
+    lam[tid] = ss;
+  }
+  __syncthreads();
+  for (int e = tid; e < N * N; e += 512) {
+    const int j = e >> 6, r = e & 63;
+    const double sg = sqrt(lam[j]);
+    V[j * N + perm[r]] = sg > 0.0 ? A[e] / sg : 0.0;
+  }
+  __syncthreads();
+  return sweeps;
+}
+
 // A = G (col-major), V = I: the Jacobi starting point (one CTA per column)
 __global__ void k_fill_gram(const double* __restrict__ G, int p, double* A, double* V) {
   const int c = blockIdx.x;
@@ -781,7 +890,23 @@ __global__ void __launch_bounds__(NT) k_init_block(
   lam = U + pp;
   ord = reinterpret_cast<int*>(lam + p);
   int sweeps;
-  if (presolved_sweeps) {  // A, V already rotated by k_jacobi_grid
+  bool lam_ready = false;
+  if constexpr (SMEM && NT == 512) {
+    if (p == 64 && !presolved_sweeps) {
+      __shared__ int permv[64];
+      sweeps = init_eig64_precond(G, A, V, U, lam, permv, &S.flag);
+      lam_ready = true;
+    }
+  }
+  if (lam_ready) {
+    // eigenvalues ready: descending order with index tie-break
+    for (int j = threadIdx.x; j < p; j += blockDim.x) {
+      int rk = 0;
+      for (int l = 0; l < p; ++l) rk += (lam[l] > lam[j]) || (lam[l] == lam[j] && l < j);
+      ord[rk] = j;
+    }
+    __syncthreads();
+  } else if (presolved_sweeps) {  // A, V already rotated by k_jacobi_grid
     sweeps = *presolved_sweeps;
   } else {
     for (int64_t e = threadIdx.x; e < pp; e += blockDim.x) {
@@ -792,7 +917,7 @@ __global__ void __launch_bounds__(NT) k_init_block(
     __syncthreads();
     sweeps = jacobi_sweeps(A, V, p, p, &S.flag);
   }
-  column_order(A, p, p, lam, ord, true);  // |G v_j| = lambda_j
+  if (!lam_ready) column_order(A, p, p, lam, ord, true);  // |G v_j| = lambda_j
   const double l0 = lam[ord[0]];
   // kept directions: sqrt(l) > 1e-12 sqrt(l0) and above the Gram floor; at most ncols
   if (threadIdx.x == 0) {
