@@ -165,6 +165,13 @@ struct SelectState {
   long long need;  // members still to take at/below the current prefix
 };
 
+__global__ void k_select_init(SelectState* st, long long need) {
+  if (threadIdx.x == 0) {
+    st->prefix = 0ull;
+    st->need = need;
+  }
+}
+
 __global__ void k_key_hist(const double* __restrict__ r, int64_t m, const SelectState* st,
                            unsigned long long prefix_arg, int shift, long long* hist) {
   __shared__ unsigned int h[256];
@@ -452,13 +459,12 @@ extern "C" int sbo_worst_set(const double* residual_sq, int64_t m, int64_t w, in
   const int64_t ntiles = ceil_div(m, kSumTile);
   long long* eq = gt + ntiles;
   const long long take = w < m ? w : m;
-  SelectState init{0ull, take};
-  SBO_CHECK_CUDA(cudaMemcpyAsync(S, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  // state set by a kernel, not a host copy: capturable in a CUDA graph and no
+  // pageable transfer competing with other streams' copies
+  k_select_init<<<1, 32, 0, st>>>(S, take);
   SBO_CHECK_CUDA(cudaMemsetAsync(hist, 0, sizeof(long long) * 256, st));
   if (w >= m) {
-    // everything: threshold 0 and all zero-keys taken
-    SelectState all{0ull, m};
-    SBO_CHECK_CUDA(cudaMemcpyAsync(S, &all, sizeof(all), cudaMemcpyHostToDevice, st));
+    // everything: threshold 0 and all zero-keys taken (need = m, prefix 0)
   } else {
     const int grid = static_cast<int>(ceil_div(m, 256) < 1184 ? ceil_div(m, 256) : 1184);
     for (int shift = 56; shift >= 0; shift -= 8) {

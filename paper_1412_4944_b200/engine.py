@@ -504,7 +504,7 @@ class Engine:
         tot = self.comm.allreduce(self.state.total.clone())
         return math.sqrt(max(float(tot.item()), 0.0) / (self.p * self.m_total))
 
-    def iterate(self, w: int, rounds: int, draws: np.ndarray, timer=None,
+    def iterate(self, w: int, rounds: int, draws, timer=None,
                 force_new_block: np.ndarray | None = None) -> IterationOut:
         """One SBO iteration (sbo.py:352-397) entering with self.K blocks.
 
@@ -512,6 +512,13 @@ class Engine:
         block trained, represent #1, retrain, represent #2.  ``force_new_block``
         (tests only) replaces the trained new block — teacher forcing past a
         rank-deficient Procrustes step, whose polar factor is not unique."""
+        dev_out = self.iterate_device(w, rounds, draws, timer, force_new_block)
+        return self.finish_iteration(dev_out)
+
+    def iterate_device(self, w: int, rounds: int, draws, timer=None,
+                       force_new_block: np.ndarray | None = None) -> dict:
+        """The device work of one iteration, with no host synchronisation (CUDA-graph
+        capturable on one GPU when ``draws`` is already a device tensor)."""
         mark = timer.mark if timer is not None else (lambda: None)
         mark()
         K0 = self.K
@@ -543,14 +550,47 @@ class Engine:
         # represent #2 (sbo.py:389-394)
         self.represent_full()
         mark()
+        return {"status": st, "counts": counts, "members": members, "n": n, "K": self.K}
+
+    def finish_iteration(self, d: dict) -> IterationOut:
+        """Host side of an iteration: RMSE, status checks, empty-block list."""
+        self.K = d["K"]
         rmse = self.rmse()
-        stc = st.cpu().numpy()
-        cnt = counts.cpu().numpy()
+        stc = d["status"].cpu().numpy()
+        cnt = d["counts"].cpu().numpy()
         # Jacobi sweeps / Newton-Schulz iterations per (phase, round, block)
         self.last_sweeps = (stc >> 8) & 0xFF
         check_status(stc)
         empty = [b for b in range(self.K) if cnt[b] == 0]
-        return IterationOut(self.K, rmse, empty, members[:n])
+        return IterationOut(self.K, rmse, empty, d["members"][: d["n"]])
+
+    def capture_iteration(self, snapshot: dict, w: int, rounds: int, draws_dev: torch.Tensor):
+        """CUDA graph of (restore the snapshot; one iteration's device work) for
+        repeated iterations from the same entering state on one GPU (the bench):
+        replaying it removes the host launch gaps between the ~100 kernels.
+        Returns replay() -> IterationOut."""
+        if self.comm.world > 1:
+            raise ValueError("graph capture is single-GPU (the sharded path has host exchanges)")
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):  # warm-up: scratch sizes, kernel attributes
+            for _ in range(2):
+                self.restore(snapshot)
+                self.iterate_device(w, rounds, draws_dev)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        torch.cuda.synchronize(self.dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.restore(snapshot)
+            out = self.iterate_device(w, rounds, draws_dev)
+        torch.cuda.synchronize(self.dev)
+
+        def replay() -> IterationOut:
+            graph.replay()
+            return self.finish_iteration(out)
+
+        replay.graph = graph
+        return replay
 
 
 def check_status(st: np.ndarray):
