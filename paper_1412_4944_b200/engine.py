@@ -564,6 +564,26 @@ class Engine:
         empty = [b for b in range(self.K) if cnt[b] == 0]
         return IterationOut(self.K, rmse, empty, d["members"][: d["n"]])
 
+    def capture(self, fn, prepare):
+        """CUDA graph of ``fn()`` (device work only) after two eager warm-up runs on a
+        side stream, each preceded by ``prepare()``; ``prepare()`` also runs once
+        before the capture.  Returns (graph, the value fn returned while captured)."""
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                prepare()
+                fn()
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        torch.cuda.synchronize(self.dev)
+        prepare()
+        torch.cuda.synchronize(self.dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            out = fn()
+        torch.cuda.synchronize(self.dev)
+        return graph, out
+
     def capture_iteration(self, snapshot: dict, w: int, rounds: int, draws_dev: torch.Tensor):
         """CUDA graph of (restore the snapshot; one iteration's device work) for
         repeated iterations from the same entering state on one GPU (the bench):
