@@ -430,3 +430,25 @@ def test_iteration_other_shapes_against_oracle(dev, p, K, s0, m):
     np.testing.assert_allclose(eng.state.residual.cpu().numpy(), tr.rep2.residual_sq,
                                rtol=1e-9, atol=1e-12)
     assert out.rmse == pytest.approx(tr.rmse, rel=1e-10)
+
+
+def test_graph_replayed_iteration_matches_eager(dev):
+    """The bench's CUDA-graph step (restore + Engine.iterate_device) gives the same
+    blocks, assignment, residuals and RMSE as an eager iteration, on every replay."""
+    from paper_1412_4944_b200 import signals
+    g = golden("gauss_iteration")
+    y32 = signals.gaussian_signals(64, 16384, seed=5)
+    eng = _engine(dev, y32, list(g["entering"]))
+    K = eng.K
+    snap = eng.snapshot()
+    draws = _block_rng(0, 1, K).standard_normal((64 + 8, 64))
+    ref = eng.iterate(1024, 6, draws)
+    want = (eng.blocks[: eng.K].cpu().numpy(), eng.state.best.cpu().numpy(),
+            eng.state.residual.cpu().numpy())
+    replay = eng.capture_iteration(snap, 1024, 6, torch.from_numpy(draws).to(dev))
+    for _ in range(2):
+        out = replay()
+        np.testing.assert_array_equal(eng.blocks[: eng.K].cpu().numpy(), want[0])
+        np.testing.assert_array_equal(eng.state.best.cpu().numpy(), want[1])
+        np.testing.assert_array_equal(eng.state.residual.cpu().numpy(), want[2])
+        assert out.rmse == ref.rmse and out.K == ref.K
