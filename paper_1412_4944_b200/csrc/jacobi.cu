@@ -490,14 +490,23 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
     const double* Xr = X0 + (cur * NC + r) * SZ;                    // this CTA's slice
     const double* Xw = X0 + (cur * NC + (8 * warp) / W) * SZ + (8 * warp) % W;  // columns 8 warp ..
     // G[16r + 8a + g][8 warp + 2 t4 + h] = sum_k X[k][16r + 8a + g] X[k][8 warp + 2 t4 + h]
-    double gg[A2][2];
+    // K split in two halves with separate accumulators: chains of 8 DMMAs, not 16
+    double gg[A2][2], gh[A2][2];
 #pragma unroll
-    for (int a2 = 0; a2 < A2; ++a2) gg[a2][0] = gg[a2][1] = 0.0;
+    for (int a2 = 0; a2 < A2; ++a2) gg[a2][0] = gg[a2][1] = gh[a2][0] = gh[a2][1] = 0.0;
 #pragma unroll 4
-    for (int k0 = 0; k0 < N; k0 += 4) {
-      const double bv = Xw[(k0 + t4) * SL + g];
+    for (int k0 = 0; k0 < N / 2; k0 += 4) {
+      const double bv = Xw[(k0 + t4) * SL + g], bw = Xw[(k0 + N / 2 + t4) * SL + g];
 #pragma unroll
-      for (int a2 = 0; a2 < A2; ++a2) dmma64(gg[a2][0], gg[a2][1], Xr[(k0 + t4) * SL + 8 * a2 + g], bv);
+      for (int a2 = 0; a2 < A2; ++a2) {
+        dmma64(gg[a2][0], gg[a2][1], Xr[(k0 + t4) * SL + 8 * a2 + g], bv);
+        dmma64(gh[a2][0], gh[a2][1], Xr[(k0 + N / 2 + t4) * SL + 8 * a2 + g], bw);
+      }
+    }
+#pragma unroll
+    for (int a2 = 0; a2 < A2; ++a2) {
+      gg[a2][0] += gh[a2][0];
+      gg[a2][1] += gh[a2][1];
     }
     const int gj = 8 * warp + 2 * t4;
     double dsum = 0.0;
@@ -516,15 +525,23 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
     const double part = block_sum<kJacobiThreads>(dsum, red);  // (syncs: As complete)
     l = fmin(1.0, al * l * (3.0 - al * al * l * l) * 0.5);
     // X'[8 warp + g][16r + 8a + 2 t4 + h] = sum_j X[8 warp + g][j] A[j][16r + 8a + 2 t4 + h]
-    double yy[A2][2];
+    double yy[A2][2], yh[A2][2];
 #pragma unroll
-    for (int a2 = 0; a2 < A2; ++a2) yy[a2][0] = yy[a2][1] = 0.0;
+    for (int a2 = 0; a2 < A2; ++a2) yy[a2][0] = yy[a2][1] = yh[a2][0] = yh[a2][1] = 0.0;
 #pragma unroll 4
-    for (int k0 = 0; k0 < N; k0 += 4) {
+    for (int k0 = 0; k0 < N / 2; k0 += 4) {
       const double av = *at(cur, 8 * warp + g, k0 + t4);
+      const double aw = *at(cur, 8 * warp + g, k0 + N / 2 + t4);
 #pragma unroll
-      for (int a2 = 0; a2 < A2; ++a2)
+      for (int a2 = 0; a2 < A2; ++a2) {
         dmma64(yy[a2][0], yy[a2][1], av, As[(k0 + t4) * AL + 8 * a2 + g]);
+        dmma64(yh[a2][0], yh[a2][1], aw, As[(k0 + N / 2 + t4) * AL + 8 * a2 + g]);
+      }
+    }
+#pragma unroll
+    for (int a2 = 0; a2 < A2; ++a2) {
+      yy[a2][0] += yh[a2][0];
+      yy[a2][1] += yh[a2][1];
     }
     const int nxt = cur ^ 1;
     double* mine = X0 + (nxt * NC + r) * SZ;
