@@ -264,6 +264,22 @@ int sbo_key_histogram(const double* residual_sq, int64_t m, uint64_t prefix, int
 int sbo_worst_collect(const double* residual_sq, int64_t m, uint64_t threshold_key,
                       int64_t take_equal, int32_t* members, int64_t* count, void* ws,
                       size_t ws_bytes, void* stream);
+/* Device-resident form of the sharded select (no host round trip): begin sets
+ * the state in ws (need = global worst-set size); per shift 56, 48, .., 0 the
+ * caller runs select_hist, allreduces hist256 across ranks (device memory,
+ * NCCL) and runs select_pick; select_counts writes this rank's (greater, equal)
+ * counts against the threshold to gt_eq[2]; the caller allgathers gt_eq[1]
+ * into eq_all[world]; select_write keeps the threshold ties of lower ranks
+ * first (dist.equal_quota) and writes the members and their count[1]. */
+int sbo_select_begin(void* ws, int64_t need, void* stream);
+int sbo_select_hist(const double* residual_sq, int64_t m, void* ws, int shift, int64_t* hist256,
+                    void* stream);
+int sbo_select_pick(void* ws, int64_t* hist256, int shift, void* stream);
+int sbo_select_counts(const double* residual_sq, int64_t m, void* ws, size_t ws_bytes,
+                      int64_t* gt_eq, void* stream);
+int sbo_select_write(const double* residual_sq, int64_t m, void* ws, size_t ws_bytes,
+                     const int64_t* gt_eq, const int64_t* eq_all, int rank, int32_t* members,
+                     int64_t* count, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Deterministic float64 sum (fixed tree) — sbo.py:295-296 (_rmse numerator).

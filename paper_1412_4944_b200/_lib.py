@@ -54,6 +54,11 @@ _SIGS = {
     "sbo_worst_set": (I, [P, I64, I64, P, P, SZ, P]),
     "sbo_key_histogram": (I, [P, I64, C.c_uint64, I, P, P]),
     "sbo_worst_collect": (I, [P, I64, C.c_uint64, I64, P, P, P, SZ, P]),
+    "sbo_select_begin": (I, [P, I64, P]),
+    "sbo_select_hist": (I, [P, I64, P, I, P, P]),
+    "sbo_select_pick": (I, [P, P, I, P]),
+    "sbo_select_counts": (I, [P, I64, P, SZ, P, P]),
+    "sbo_select_write": (I, [P, I64, P, SZ, P, P, I, P, P, P]),
     "sbo_sum_workspace_bytes": (SZ, [I64]),
     "sbo_sum": (I, [P, I64, P, P, SZ, P]),
     "sbo_defect": (I, [P, I, I, P, P]),

@@ -481,6 +481,82 @@ extern "C" int sbo_worst_set(const double* residual_sq, int64_t m, int64_t w, in
   return check_launch("k_worst_*");
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident radix select for signal shards (the sharded worst set): the
+// select state lives in the worst-set workspace; the caller allreduces each
+// pass's histogram in device memory (NCCL) between sbo_select_hist and
+// sbo_select_pick, and allgathers the per-rank tie counts before
+// sbo_select_write — no host round trip.
+// ---------------------------------------------------------------------------
+__global__ void k_select_take(SelectState* st, const long long* eq_all, int rank,
+                              const long long* gt_eq, long long* count) {
+  if (threadIdx.x == 0) {
+    long long before = 0;
+    for (int q = 0; q < rank; ++q) before += eq_all[q];
+    long long take = st->need - before;  // threshold ties go to lower ranks first
+    if (take < 0) take = 0;
+    if (take > eq_all[rank]) take = eq_all[rank];
+    st->need = take;
+    *count = gt_eq[0] + take;
+  }
+}
+
+extern "C" int sbo_select_begin(void* ws, int64_t need, void* stream) {
+  k_select_init<<<1, 32, 0, as_stream(stream)>>>(static_cast<SelectState*>(ws), need);
+  return check_launch("k_select_init");
+}
+
+extern "C" int sbo_select_hist(const double* residual_sq, int64_t m, void* ws, int shift,
+                               int64_t* hist256, void* stream) {
+  if (shift < 0 || shift > 56 || shift % 8) return fail(SBO_EINVAL, "shift must be 0, 8, .., 56");
+  cudaStream_t st = as_stream(stream);
+  SBO_CHECK_CUDA(cudaMemsetAsync(hist256, 0, sizeof(int64_t) * 256, st));
+  if (m == 0) return SBO_OK;
+  const int grid = static_cast<int>(ceil_div(m, 256) < 1184 ? ceil_div(m, 256) : 1184);
+  k_key_hist<<<grid, 256, 0, st>>>(residual_sq, m, static_cast<const SelectState*>(ws), 0ull,
+                                   shift, reinterpret_cast<long long*>(hist256));
+  return check_launch("k_key_hist");
+}
+
+extern "C" int sbo_select_pick(void* ws, int64_t* hist256, int shift, void* stream) {
+  k_key_pick<<<1, 256, 0, as_stream(stream)>>>(static_cast<SelectState*>(ws),
+                                               reinterpret_cast<long long*>(hist256), shift);
+  return check_launch("k_key_pick");
+}
+
+extern "C" int sbo_select_counts(const double* residual_sq, int64_t m, void* ws, size_t ws_bytes,
+                                 int64_t* gt_eq, void* stream) {
+  if (ws_bytes < sbo_worst_workspace_bytes(m)) return fail(SBO_EINVAL, "worst workspace too small");
+  cudaStream_t st = as_stream(stream);
+  SelectState* S = static_cast<SelectState*>(ws);
+  long long* gt = reinterpret_cast<long long*>(S + 1) + 256;
+  const int64_t ntiles = ceil_div(m > 0 ? m : 1, kSumTile);
+  long long* eq = gt + ntiles;
+  if (m == 0) return cudaMemsetAsync(gt_eq, 0, 2 * sizeof(int64_t), st) == cudaSuccess ? SBO_OK
+                                                                                : fail(SBO_ECUDA, "memset");
+  k_worst_count<<<static_cast<unsigned>(ntiles), kSumTile, 0, st>>>(residual_sq, m, S, 0ull, gt, eq);
+  k_worst_scan<<<1, 1024, 0, st>>>(gt, eq, ntiles, reinterpret_cast<long long*>(gt_eq));
+  return check_launch("k_worst_count/scan");
+}
+
+extern "C" int sbo_select_write(const double* residual_sq, int64_t m, void* ws, size_t ws_bytes,
+                                const int64_t* gt_eq, const int64_t* eq_all, int rank,
+                                int32_t* members, int64_t* count, void* stream) {
+  if (ws_bytes < sbo_worst_workspace_bytes(m)) return fail(SBO_EINVAL, "worst workspace too small");
+  cudaStream_t st = as_stream(stream);
+  SelectState* S = static_cast<SelectState*>(ws);
+  long long* gt = reinterpret_cast<long long*>(S + 1) + 256;
+  const int64_t ntiles = ceil_div(m > 0 ? m : 1, kSumTile);
+  long long* eq = gt + ntiles;
+  k_select_take<<<1, 32, 0, st>>>(S, reinterpret_cast<const long long*>(eq_all), rank,
+                                  reinterpret_cast<const long long*>(gt_eq),
+                                  reinterpret_cast<long long*>(count));
+  if (m > 0)
+    k_worst_write<<<static_cast<unsigned>(ntiles), kSumTile, 0, st>>>(residual_sq, m, S, 0ull, 0,
+                                                                      gt, eq, members);
+  return check_launch("k_worst_write");
+}
+
 extern "C" int sbo_key_histogram(const double* residual_sq, int64_t m, uint64_t prefix, int shift,
                                  int64_t* hist256, void* stream) {
   if (shift < 0 || shift > 56 || shift % 8) return fail(SBO_EINVAL, "shift must be 0, 8, .., 56");

@@ -52,6 +52,9 @@ class Comm:
     def allgather_int(self, v: int) -> list[int]:
         return [v]
 
+    def allgather(self, t):
+        return t
+
 
 class TorchComm(Comm):
     """NCCL (or gloo) process group of torch.distributed."""
@@ -70,6 +73,17 @@ class TorchComm(Comm):
             return t
         self.dist.all_reduce(t, group=self.group)
         return t
+
+    def allgather(self, t):
+        """Concatenation over ranks of a 1-D tensor (device-resident on NCCL)."""
+        if t.is_cuda and self.dist.get_backend(self.group) != "nccl":
+            h = t.cpu()
+            out = [torch.zeros_like(h) for _ in range(self.world)]
+            self.dist.all_gather(out, h, group=self.group)
+            return torch.cat(out).to(t.device)
+        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return out
 
     def allgather_int(self, v):
         t = torch.tensor([v], dtype=torch.int64, device=_comm_device(self.dist))
@@ -628,31 +642,29 @@ def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int]:
 
     Keys are the float64 bit patterns of residual_sq (order-preserving for >= 0);
     ties at the threshold go to the lowest GLOBAL signal index, i.e. to lower
-    ranks first (contiguous column shards)."""
-    from .dist import equal_quota, select_threshold
-
+    ranks first (contiguous column shards) — dist.equal_quota's rule, applied on
+    the device.  The select state, the eight histograms and the tie counts stay in
+    device memory (collectives stream-ordered on NCCL); the one host read is the
+    local member count, which sizes the Gram and segment launches."""
     res = eng.state.residual
-    hist = torch.zeros(256, dtype=torch.int64, device=eng.dev)
-
-    def local_hist(prefix: int, shift: int) -> np.ndarray:
-        hist.zero_()
-        eng._call("sbo_key_histogram", res.data_ptr(), eng.m, prefix, shift, hist.data_ptr(),
-                  eng.stream)
-        return hist.cpu().numpy()
-
-    def allreduce(h: np.ndarray) -> np.ndarray:
-        t = torch.from_numpy(h).to(eng.dev)
-        return eng.comm.allreduce(t).cpu().numpy()
-
-    prefix, need_eq = select_threshold(local_hist, allreduce, min(w, eng.m_total))
-    cnt = torch.zeros(2, dtype=torch.int64, device=eng.dev)
+    need = min(w, eng.m_total)
     members = torch.empty(max(eng.m, 1), dtype=torch.int32, device=eng.dev)
+    if need < 1:
+        return members, 0
     ws = eng.scratch.get("worst", L.size("sbo_worst_workspace_bytes", eng.m))
-    # first pass: counts only (take 0 equal keys) to learn this rank's equal count
-    eng._call("sbo_worst_collect", res.data_ptr(), eng.m, prefix, 0, members.data_ptr(),
-              cnt.data_ptr(), ws.data_ptr(), ws.numel(), eng.stream)
-    gt, eq = (int(x) for x in cnt.cpu().numpy())
-    take = equal_quota(eng.comm.allgather_int(eq), eng.comm.rank, need_eq)
-    eng._call("sbo_worst_collect", res.data_ptr(), eng.m, prefix, take, members.data_ptr(),
-              cnt.data_ptr(), ws.data_ptr(), ws.numel(), eng.stream)
-    return members, gt + take
+    hist = torch.empty(256, dtype=torch.int64, device=eng.dev)
+    eng._call("sbo_select_begin", ws.data_ptr(), need, eng.stream)
+    for shift in range(56, -8, -8):
+        eng._call("sbo_select_hist", res.data_ptr(), eng.m, ws.data_ptr(), shift,
+                  hist.data_ptr(), eng.stream)
+        eng.comm.allreduce(hist)
+        eng._call("sbo_select_pick", ws.data_ptr(), hist.data_ptr(), shift, eng.stream)
+    gt_eq = torch.empty(2, dtype=torch.int64, device=eng.dev)
+    eng._call("sbo_select_counts", res.data_ptr(), eng.m, ws.data_ptr(), ws.numel(),
+              gt_eq.data_ptr(), eng.stream)
+    eq_all = eng.comm.allgather(gt_eq[1:2].clone())
+    count = torch.empty(1, dtype=torch.int64, device=eng.dev)
+    eng._call("sbo_select_write", res.data_ptr(), eng.m, ws.data_ptr(), ws.numel(),
+              gt_eq.data_ptr(), eq_all.data_ptr(), eng.comm.rank, members.data_ptr(),
+              count.data_ptr(), eng.stream)
+    return members, int(count.item())
