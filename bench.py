@@ -455,98 +455,103 @@ def run_ours(a):
 
 
 def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
-    """Same metric through the host-buffer path: every step uploads its signals (from
-    pinned host memory) and entering state, runs the iteration, and reads the new
-    dictionary and assignment back.  The signal upload of step i+1 runs on a copy
-    stream while step i computes (two device signal buffers), as a training loop over
-    streamed data would; every copy is inside the timed region."""
+    """Same metric through the host-buffer path: every step uploads its signals and
+    entering state (from pinned host memory), runs the iteration, and reads the new
+    dictionary, assignment and residuals back; every copy is inside the timed region.
+    Step i+1's uploads run on a copy stream while step i computes, as a training loop
+    over streamed data would: two device signal buffers and two device staging sets
+    for the entering state (restored into the live state by a device copy at the
+    step's start), and the outputs leave through a device staging set on a third
+    stream, so no host transfer sits on the compute stream."""
     import torch
     st = eng.state
     host_y = torch.from_numpy(rows).pin_memory()
     host_blocks = snap_blocks[:K0].cpu().pin_memory()
     host_state = [t.cpu().pin_memory() for t in snap]
+    host_draws = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).pin_memory()
     out_blocks = torch.empty((K0 + 1,) + tuple(snap_blocks.shape[1:]), dtype=torch.float64).pin_memory()
     out_best = torch.empty(rows.shape[0], dtype=torch.int32).pin_memory()
     out_res = torch.empty(rows.shape[0], dtype=torch.float64).pin_memory()
     h2d = host_y.numel() * 4 + host_blocks.numel() * 8 + sum(t.numel() * t.element_size()
                                                             for t in host_state)
-    h2d += int(np.asarray(draws).size) * 8  # the new block's completion draws
+    h2d += host_draws.numel() * 8  # the new block's completion draws
     d2h = out_blocks.numel() * 8 + out_best.numel() * 4 + out_res.numel() * 8
-    # both on created streams: work on the legacy default stream would serialise
-    # with the copy stream
+    # all on created streams: work on the legacy default stream would serialise
+    # with the copy streams
     compute = torch.cuda.Stream(eng.dev)
     copier = torch.cuda.Stream(eng.dev)
+    reader = torch.cuda.Stream(eng.dev)
     ybuf = [eng.sig.y, torch.empty_like(eng.sig.y)]
-    copied = [torch.cuda.Event(), torch.cuda.Event()]
-    freed = [None, None]
+    entering = eng.snapshot()
+    stg = [entering, {"K": K0, "exact_scores": True, "blocks": entering["blocks"].clone(),
+                      "state": [t.clone() for t in entering["state"]]}]
+    for sg in stg:
+        sg["K"], sg["exact_scores"] = K0, True
+    dev_draws = [torch.empty(host_draws.shape, dtype=torch.float64, device=eng.dev)
+                 for _ in range(2)]
+    out_dev = [torch.empty((K0 + 1,) + tuple(snap_blocks.shape[1:]), dtype=torch.float64,
+                           device=eng.dev), torch.empty_like(st.best), torch.empty_like(st.residual)]
+    ready = [torch.cuda.Event(), torch.cuda.Event()]   # step j's inputs are on the device
+    freed = [None, None]                               # the last step using set j is done
+    read_done = [None]                                 # out_dev is free again
 
     def upload(j):
+        """Entering state + signals of a step into set j (copy stream)."""
         with torch.cuda.stream(copier):
             if freed[j] is not None:
-                copier.wait_event(freed[j])  # the step that last read ybuf[j] is done
-            ybuf[j].copy_(host_y, non_blocking=True)
-            copied[j].record(copier)
-
-    host_draws = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).pin_memory()
-    dev_draws = torch.empty(host_draws.shape, dtype=torch.float64, device=eng.dev)
-
-    state_ready = torch.cuda.Event()
-    last_done = [None]
-
-    def stage_state():
-        # the step's state upload goes on the copy stream too, ahead of the next
-        # step's signal upload: host-to-device copies from two streams share a copy
-        # engine, and a small copy issued on the compute stream while the big one
-        # runs would wait for all of it
-        with torch.cuda.stream(copier):
-            if last_done[0] is not None:
-                copier.wait_event(last_done[0])  # the previous step is done with the state
-            eng.blocks[:K0].copy_(host_blocks, non_blocking=True)
-            for dst, src in zip((st.best, st.score, st.norm, st.residual, st.total),
-                                host_state):
+                copier.wait_event(freed[j])
+            stg[j]["blocks"][:K0].copy_(host_blocks, non_blocking=True)
+            for dst, src in zip(stg[j]["state"], host_state):
                 dst.copy_(src, non_blocking=True)
-            dev_draws.copy_(host_draws, non_blocking=True)
-            state_ready.record(copier)
+            dev_draws[j].copy_(host_draws, non_blocking=True)
+            ybuf[j].copy_(host_y, non_blocking=True)
+            ready[j].record(copier)
 
-    # one GPU: each signal buffer's step (operand split + iteration) as a CUDA graph
+    def device_step(j):
+        eng.restore(stg[j])
+        eng.refresh_signals()  # device-side operand split of the uploaded signals
+        return eng.iterate_device(w, a.rounds, dev_draws[j])
+
+    # one GPU: each set's step (restore + operand split + iteration) as a CUDA graph
     graphs = [None, None]
     if dist is None and os.environ.get("SBO_BENCH_NO_GRAPH", "0") != "1":
-        entering = eng.snapshot()
-        entering["blocks"][:K0].copy_(host_blocks.to(eng.dev))
-        for dst, src in zip(entering["state"], host_state):
-            dst.copy_(src.to(eng.dev))
-        entering["K"], entering["exact_scores"] = K0, True
-        dev_draws.copy_(host_draws.to(eng.dev))
         for j in range(2):
+            stg[j]["blocks"][:K0].copy_(host_blocks.to(eng.dev))
+            for dst, src in zip(stg[j]["state"], host_state):
+                dst.copy_(src.to(eng.dev))
+            dev_draws[j].copy_(host_draws.to(eng.dev))
             eng.sig.y = ybuf[j]
-            graphs[j] = eng.capture(
-                lambda: (eng.refresh_signals(), eng.iterate_device(w, a.rounds, dev_draws))[1],
-                lambda: eng.restore(entering))
+            graphs[j] = eng.capture(lambda j=j: device_step(j), lambda: None)
         eng.sig.y = ybuf[0]
 
     def step(j):
-        compute.wait_event(state_ready)
-        compute.wait_event(copied[j])
+        compute.wait_event(ready[j])
         eng.sig.y = ybuf[j]
+        eng.K = K0
         if graphs[j] is not None:
-            eng.K = K0
             graphs[j][0].replay()
-            eng.finish_iteration(graphs[j][1])
+            out = graphs[j][1]
         else:
-            eng.refresh_signals()  # device-side operand split of the uploaded signals
-            eng.K = K0
-            eng.exact_scores = True  # the uploaded state is a full representation's
-            eng.iterate(w, a.rounds, dev_draws)
-        out_blocks.copy_(eng.blocks[: K0 + 1], non_blocking=True)
-        out_best.copy_(st.best, non_blocking=True)
-        out_res.copy_(st.residual, non_blocking=True)
+            out = device_step(j)
         freed[j] = torch.cuda.Event()
         freed[j].record(compute)
-        last_done[0] = freed[j]
+        if read_done[0] is not None:
+            compute.wait_event(read_done[0])
+        out_dev[0].copy_(eng.blocks[: K0 + 1])
+        out_dev[1].copy_(st.best)
+        out_dev[2].copy_(st.residual)
+        staged = torch.cuda.Event()
+        staged.record(compute)
+        with torch.cuda.stream(reader):
+            reader.wait_event(staged)
+            for dst, src in zip((out_blocks, out_best, out_res), out_dev):
+                dst.copy_(src, non_blocking=True)
+            read_done[0] = torch.cuda.Event()
+            read_done[0].record(reader)
+        eng.finish_iteration(out)
 
     torch.cuda.synchronize()
     with torch.cuda.stream(compute):
-        stage_state()
         upload(0)
         step(0)  # warm-up
         torch.cuda.synchronize()
@@ -559,7 +564,6 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
         dbg = os.environ.get("SBO_E2E_DEBUG") == "1"
         for i in range(a.steps):
             t0 = time.perf_counter()
-            stage_state()
             if i + 1 < a.steps:
                 upload((i + 1) % 2)  # overlaps step i
             t1 = time.perf_counter()
@@ -570,6 +574,7 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
                 ev.synchronize()
                 print(f"e2e step {i}: issue {1e3 * (t1 - t0):.2f} ms, step {1e3 * (time.perf_counter() - t1):.2f} ms, "
                       f"since start {s.elapsed_time(ev):.2f} ms", file=sys.stderr)
+        compute.wait_event(read_done[0])  # the last step's results are on the host
         e.record(compute)
     torch.cuda.synchronize()
     eng.sig.y = ybuf[0]
@@ -577,7 +582,8 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
     m_total = eng.m_total
     return {"value": m_total / t, "unit": "signals/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
-            "pipelining": "signal upload of step i+1 overlaps step i (copy stream)"}
+            "pipelining": "step i+1's signal and state uploads overlap step i (copy stream); "
+                          "results leave through a device staging copy on a third stream"}
 
 
 def main():
