@@ -408,9 +408,11 @@ def run_ours(a):
                      axis=0)
 
     # e2e: host buffers through the public engine API, copies inside the timed region
-    e2e = None
+    e2e = e2e_ingest = None
     if not a.no_e2e:
         e2e = run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist if world > 1 else None)
+        e2e_ingest = run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws,
+                             dist if world > 1 else None, ingest=shard_corners(a, rank, world))
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -446,6 +448,7 @@ def run_ours(a):
                                "t_roof_ms": t_roof * 1e3, "frac": t_roof / t_step,
                                "model": "SURVEY.md 8(d): max(F/TF32 peak, B/HBM)"},
         "e2e": e2e,
+        "e2e_ingest": e2e_ingest,
         "cpu_baseline": cpu,
         "rmse": out.rmse,
     }
@@ -454,7 +457,16 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
-def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
+def shard_corners(a, rank, world):
+    """This rank's patch corners (data.py:199-201 draws over the whole workload)."""
+    from paper_1412_4944_b200 import data, signals
+    grid = signals.scene(a.scene, a.scene, 0)
+    r, c = data.patch_corners(a.scene, a.scene, a.p_edge, a.m * world, 11)
+    lo, hi = rank * a.m, (rank + 1) * a.m
+    return grid, r[lo:hi].astype(np.int32), c[lo:hi].astype(np.int32)
+
+
+def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
     """Same metric through the host-buffer path: every step uploads its signals and
     entering state (from pinned host memory), runs the iteration, and reads the new
     dictionary, assignment and residuals back; every copy is inside the timed region.
@@ -462,18 +474,27 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
     over streamed data would: two device signal buffers and two device staging sets
     for the entering state (restored into the live state by a device copy at the
     step's start), and the outputs leave through a device staging set on a third
-    stream, so no host transfer sits on the compute stream."""
+    stream, so no host transfer sits on the compute stream.
+
+    ``ingest`` = (grid, rows, cols): the step's input is the 8-bit scene and this
+    rank's int32 patch corners instead of the float32 signal matrix; the patches are
+    extracted on the device at the start of the step (data.extract_rows, the
+    device form of data.py:182-208)."""
     import torch
+    from paper_1412_4944_b200 import data as D
     st = eng.state
-    host_y = torch.from_numpy(rows).pin_memory()
+    if ingest is None:
+        host_in = [torch.from_numpy(rows).pin_memory()]
+    else:
+        host_in = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in ingest]
     host_blocks = snap_blocks[:K0].cpu().pin_memory()
     host_state = [t.cpu().pin_memory() for t in snap]
     host_draws = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).pin_memory()
     out_blocks = torch.empty((K0 + 1,) + tuple(snap_blocks.shape[1:]), dtype=torch.float64).pin_memory()
     out_best = torch.empty(rows.shape[0], dtype=torch.int32).pin_memory()
     out_res = torch.empty(rows.shape[0], dtype=torch.float64).pin_memory()
-    h2d = host_y.numel() * 4 + host_blocks.numel() * 8 + sum(t.numel() * t.element_size()
-                                                            for t in host_state)
+    h2d = sum(t.numel() * t.element_size() for t in host_in) + host_blocks.numel() * 8 + \
+        sum(t.numel() * t.element_size() for t in host_state)
     h2d += host_draws.numel() * 8  # the new block's completion draws
     d2h = out_blocks.numel() * 8 + out_best.numel() * 4 + out_res.numel() * 8
     # all on created streams: work on the legacy default stream would serialise
@@ -482,6 +503,8 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
     copier = torch.cuda.Stream(eng.dev)
     reader = torch.cuda.Stream(eng.dev)
     ybuf = [eng.sig.y, torch.empty_like(eng.sig.y)]
+    dev_in = [ybuf[:1], [ybuf[1]]] if ingest is None else \
+        [[torch.empty_like(t, device=eng.dev) for t in host_in] for _ in range(2)]
     entering = eng.snapshot()
     stg = [entering, {"K": K0, "exact_scores": True, "blocks": entering["blocks"].clone(),
                       "state": [t.clone() for t in entering["state"]]}]
@@ -504,11 +527,16 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
             for dst, src in zip(stg[j]["state"], host_state):
                 dst.copy_(src, non_blocking=True)
             dev_draws[j].copy_(host_draws, non_blocking=True)
-            ybuf[j].copy_(host_y, non_blocking=True)
+            for dst, src in zip(dev_in[j], host_in):
+                dst.copy_(src, non_blocking=True)
             ready[j].record(copier)
 
     def device_step(j):
         eng.restore(stg[j])
+        if ingest is not None:  # patches of the uploaded scene, on the device
+            g, r, c = dev_in[j]
+            D.extract_rows(g, D.GRID_U8, a.p_edge, r, c, "unit-range", out=ybuf[j],
+                           stream=eng.stream)
         eng.refresh_signals()  # device-side operand split of the uploaded signals
         return eng.iterate_device(w, a.rounds, dev_draws[j])
 
@@ -520,6 +548,8 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
             for dst, src in zip(stg[j]["state"], host_state):
                 dst.copy_(src.to(eng.dev))
             dev_draws[j].copy_(host_draws.to(eng.dev))
+            for dst, src in zip(dev_in[j], host_in):
+                dst.copy_(src.to(eng.dev))
             eng.sig.y = ybuf[j]
             graphs[j] = eng.capture(lambda j=j: device_step(j), lambda: None)
         eng.sig.y = ybuf[0]
@@ -580,10 +610,14 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist):
     eng.sig.y = ybuf[0]
     t = max_over_ranks(s.elapsed_time(e) / 1e3 / a.steps, dist, eng.dev)
     m_total = eng.m_total
-    return {"value": m_total / t, "unit": "signals/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h,
-            "pipelining": "step i+1's signal and state uploads overlap step i (copy stream); "
-                          "results leave through a device staging copy on a third stream"}
+    out = {"value": m_total / t, "unit": "signals/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h,
+           "pipelining": "step i+1's input and state uploads overlap step i (copy stream); "
+                         "results leave through a device staging copy on a third stream"}
+    if ingest is not None:
+        out["input"] = ("8-bit scene + int32 patch corners per step; patches extracted on the "
+                        "device (paper_1412_4944_b200.data, data.py:182-208)")
+    return out
 
 
 def main():

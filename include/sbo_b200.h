@@ -295,6 +295,21 @@ int sbo_frobenius_sq(const void* y, int dtype, int64_t m, int p, const double* b
                      const int32_t* block, int s0, int64_t ld, const int16_t* idx,
                      const double* val, double* total, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Signal ingestion — replaces data.py:182-208 (extract_patches) after its corner
+ * draws (rows[j], cols[j]: numpy default_rng(seed).integers on the host).  Writes
+ * count rows of edge^2 entries: entry c*edge + r of row j is
+ * grid[(rows[j] + r) * ld + cols[j] + c] / 255 (float64), minus the patch mean
+ * (numpy's pairwise float64 sum / edge^2) for normalization 1
+ * ("unit-range-dc-removed").  grid_dtype: 0 uint8, 1 float64; out_dtype SBO_F32
+ * (round-to-nearest of the float64 value) or SBO_F64.  edge <= 32.  A uint8 grid
+ * is read in aligned 4-byte words: its allocation must be 4-byte aligned and
+ * padded to a multiple of 4 bytes (cudaMalloc and the torch allocator are).
+ */
+int sbo_extract_patches(const void* grid, int grid_dtype, int64_t h, int64_t w, int64_t ld,
+                        int edge, const int32_t* rows, const int32_t* cols, int64_t count,
+                        int normalization, int out_dtype, void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

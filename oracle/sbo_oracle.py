@@ -379,3 +379,56 @@ def default_workers() -> int:
     """parallel.py:16-29 (ORTHODICT_WORKERS or the CPU count)."""
     env = os.environ.get("ORTHODICT_WORKERS")
     return int(env) if env else (os.cpu_count() or 1)
+
+
+# ---------------------------------------------------------------------------
+# signal ingestion (SURVEY.md 8(f) row 3)
+# ---------------------------------------------------------------------------
+
+def pairwise_sum_rows(a: np.ndarray) -> np.ndarray:
+    """Column sums of a (n, count) float64 array in numpy's pairwise order
+    (numpy umath loops_utils.h.src, pairwise_sum; the reduction data.py:207's
+    ``mean(axis=0)`` runs over each contiguous column): plain accumulation below
+    8 terms, 8 interleaved accumulators up to 128, halving (multiples of 8) above."""
+    n = a.shape[0]
+    if n < 8:
+        res = np.zeros(a.shape[1:], np.float64)
+        for i in range(n):
+            res = res + a[i]
+        return res
+    if n <= 128:
+        r = [a[j].copy() for j in range(8)]
+        i = 8
+        while i < n - (n % 8):
+            for j in range(8):
+                r[j] = r[j] + a[i + j]
+            i += 8
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        while i < n:
+            res = res + a[i]
+            i += 1
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return pairwise_sum_rows(a[:n2]) + pairwise_sum_rows(a[n2:])
+
+
+def extract_patches(grid: np.ndarray, edge: int, count: int, seed: int,
+                    normalization: str = "unit-range") -> np.ndarray:
+    """data.py:182-208 — Fortran (edge^2, count) float64 signals of random patches:
+    corners from default_rng(seed).integers (rows, then columns; data.py:199-201),
+    column-major vectorization (entry (r, c) at c*edge + r; data.py:203-204), /255
+    (data.py:205), minus the patch mean for the dc-removed variant (data.py:206-207)."""
+    grid = np.asarray(grid)
+    h, w = grid.shape
+    rng = np.random.default_rng(seed)
+    rows = rng.integers(0, h - edge + 1, size=count)
+    cols = rng.integers(0, w - edge + 1, size=count)
+    n = edge * edge
+    y = np.empty((n, count), np.float64)
+    for c in range(edge):
+        for r in range(edge):
+            y[c * edge + r] = grid[rows + r, cols + c].astype(np.float64) / 255.0
+    if normalization == "unit-range-dc-removed":
+        y = y - pairwise_sum_rows(y) / n
+    return np.asfortranarray(y)

@@ -63,6 +63,7 @@ _SIGS = {
     "sbo_sum": (I, [P, I64, P, P, SZ, P]),
     "sbo_defect": (I, [P, I, I, P, P]),
     "sbo_frobenius_sq": (I, [P, I, I64, I, P, P, I, I64, P, P, P, P, SZ, P]),
+    "sbo_extract_patches": (I, [P, I, I64, I64, I64, I, P, P, I64, I, I, P, P]),
 }
 
 _lib = None

@@ -120,6 +120,21 @@ def _block_rng(seed: int, phase: int, ordinal: int) -> np.random.Generator:
     return np.random.default_rng(np.random.SeedSequence(entropy))
 
 
+def _device_signals(y) -> tuple[Signals, int, int]:
+    """Signals already on the device (data.extract_patches_device): validated there."""
+    if not torch.isfinite(y.y).all().item():
+        raise ValueError("signal matrix contains NaN or Inf entries")
+    return y, y.p, y.m
+
+
+def _signals(y, dev) -> tuple[Signals, int, int]:
+    """(device signals, p, m) from a host p x m matrix or device Signals."""
+    if isinstance(y, Signals):
+        return _device_signals(y)
+    y = _check_signals(y)
+    return Signals.from_reference(y, dev), y.shape[0], y.shape[1]
+
+
 def _check_signals(y) -> np.ndarray:
     y = np.asarray(y, dtype=np.float64)
     if y.ndim != 2:
@@ -164,8 +179,8 @@ def represent(y: np.ndarray, dictionary: UnionDictionary, s0: int, kind: str = "
     """sbo.py:138-220 — best block per signal (first maximum) and its top-s0 code."""
     _check_kind(kind)
     dictionary.validate()
-    y = _check_signals(y)
-    p, m = y.shape
+    dev = require_device()
+    sig, p, m = _signals(y, dev)
     if p != dictionary.p:
         raise ValueError(f"signals have dimension {p}, dictionary blocks {dictionary.p}")
     if s0 < 1:
@@ -173,8 +188,7 @@ def represent(y: np.ndarray, dictionary: UnionDictionary, s0: int, kind: str = "
     if chunk_size < 1:
         raise ValueError(f"chunk_size must be at least 1, got {chunk_size}")
     resolve_workers(workers)
-    dev = require_device()
-    eng = Engine(Signals.from_reference(y, dev), s0, kind, k_cap=dictionary.num_blocks)
+    eng = Engine(sig, s0, kind, k_cap=dictionary.num_blocks)
     eng.set_blocks(np.stack(dictionary.blocks))
     best, energy, resid, idx, val = _code_all(eng)
     k = eng.k
@@ -260,17 +274,17 @@ def _init_into(eng: Engine, cfg: SboConfig, m_total: int, local_cols=None) -> No
 def sbo_init(y: np.ndarray, cfg: SboConfig, workers: int | None = None) -> UnionDictionary:
     """sbo.py:259-292 — k0 start-up blocks, each trained on p0 sampled signals."""
     cfg.validate()
-    y = np.asarray(y, dtype=np.float64)
-    m = y.shape[1]
+    if not isinstance(y, Signals):
+        y = np.asarray(y, dtype=np.float64)
+    m = y.m if isinstance(y, Signals) else y.shape[1]
     if m < 1:
         raise ValueError("cannot initialize from an empty signal set")
     if cfg.p0 > m:
         warnings.warn(f"p0={cfg.p0} exceeds the {m} available signals; sampling with "
                       "replacement", stacklevel=2)
     resolve_workers(workers)
-    y = _check_signals(y)
-    eng = Engine(Signals.from_reference(y, require_device()), cfg.s0, cfg.energy_kind,
-                 k_cap=cfg.k0)
+    sig, _, _ = _signals(y, require_device())
+    eng = Engine(sig, cfg.s0, cfg.energy_kind, k_cap=cfg.k0)
     _init_into(eng, cfg, m)
     return UnionDictionary([q for q in eng.blocks[: cfg.k0].cpu().numpy()])
 
@@ -327,19 +341,24 @@ def sbo_train(y: np.ndarray, cfg: SboConfig, workers: int | None = None
     """sbo.py:299-420 — initialize, then grow by one block per iteration and refine,
     until the RMSE reaches target_error or the union holds k_max blocks."""
     cfg.validate()
-    y = np.asarray(y, dtype=np.float64)
-    p, m = y.shape
+    if isinstance(y, Signals):
+        p, m = y.p, y.m
+    else:
+        y = np.asarray(y, dtype=np.float64)
+        if y.ndim != 2:
+            raise ValueError(f"expected a 2-D signal matrix, got shape {y.shape}")
+        p, m = y.shape
     if m < 1:
         raise ValueError("cannot train on an empty signal set")
     nworkers = resolve_workers(workers)
-    y = _check_signals(y)
     w_size = cfg.worst_size if cfg.worst_size is not None else max(p, m // 16)
     report = TrainReport(algo="sbo", config=_config_echo(cfg, w_size), seed=cfg.seed,
                          workers=nworkers)
     if cfg.p0 > m:
         report.notes.append(f"p0={cfg.p0} exceeds m={m}; initial blocks sampled with replacement")
     dev = require_device()
-    eng = Engine(Signals.from_reference(y, dev), cfg.s0, cfg.energy_kind, k_cap=cfg.k_max)
+    sig, _, _ = _signals(y, dev)
+    eng = Engine(sig, cfg.s0, cfg.energy_kind, k_cap=cfg.k_max)
     t0 = perf_counter()
     _init_into(eng, cfg, m)
     torch.cuda.synchronize(dev)

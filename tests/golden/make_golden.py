@@ -189,13 +189,39 @@ def make_small():
     np.savez_compressed(HERE / "small_cases.npz", **out)
 
 
+INGEST_CASES = [  # (grid, edge, normalization, count, seed)
+    ("u8", 1, "unit-range", 40, 5), ("u8", 3, "unit-range-dc-removed", 50, 6),
+    ("u8", 8, "unit-range", 50, 7), ("u8", 8, "unit-range-dc-removed", 50, 8),
+    ("u8", 12, "unit-range-dc-removed", 30, 9), ("u8", 16, "unit-range", 30, 10),
+    ("u8", 16, "unit-range-dc-removed", 30, 11), ("f64", 5, "unit-range", 40, 12),
+    ("f64", 8, "unit-range-dc-removed", 40, 13),
+]
+
+
+def make_ingest():
+    """data.py:182-208 extract_patches on a small scene and a float grid (device ingestion)."""
+    grids = {"u8": rdata.synthetic_test_image(96, 80, seed=3),
+             "f64": np.random.default_rng(4).uniform(0.0, 255.0, (37, 29))}
+    import json
+    out = {"grid_u8": grids["u8"], "grid_f64": grids["f64"],
+           "cases_json": np.array(json.dumps(INGEST_CASES))}
+    for i, (g, e, norm, count, seed) in enumerate(INGEST_CASES):
+        cfg = rdata.PatchConfig(patch_edge=e, count=count, seed=seed, normalization=norm)
+        out[f"case{i}"] = rdata.extract_patches(grids[g], cfg)
+    np.savez_compressed(HERE / "ingest_patches.npz", **out)
+
+
 def main():
+    if sys.argv[1:] == ["ingest"]:
+        make_ingest()
+        return
     u8 = make_patches()
     d, y = make_represent(u8)
     make_iteration(d, y)
     make_gaussian_iteration()
     make_train(u8)
     make_small()
+    make_ingest()
     (HERE / "VERSIONS.txt").write_text(
         f"orthodict {orthodict.__version__}\nnumpy {np.__version__}\n"
         f"scipy {__import__('scipy').__version__}\n")

@@ -1,4 +1,6 @@
 """Pin the CPU oracle against fixtures produced by the real reference (CPU only)."""
+import json
+
 import numpy as np
 import pytest
 
@@ -100,3 +102,11 @@ def test_select_hand_cases():
     assert list(i[:, 0]) == [0, 1]
     i, v = O.top_support(np.array([2.0, 0.0, -1.0]), 4)
     assert list(i[:, 0]) == [0, 1, 2]
+
+
+def test_extract_patches_oracle_matches_reference():
+    """The ingestion restatement reproduces data.py:182-208 bit for bit."""
+    g = golden("ingest_patches")
+    for i, (kind, e, norm, count, seed) in enumerate(json.loads(str(g["cases_json"]))):
+        y = O.extract_patches(g[f"grid_{kind}"], e, count, seed, norm)
+        np.testing.assert_array_equal(y, g[f"case{i}"], err_msg=f"case {i}")
