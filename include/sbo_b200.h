@@ -310,6 +310,17 @@ int sbo_extract_patches(const void* grid, int grid_dtype, int64_t h, int64_t w, 
                         int edge, const int32_t* rows, const int32_t* cols, int64_t count,
                         int normalization, int out_dtype, void* out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Codes persistence — the float64 payloads of store.py:99-115 (save_sbo_codes)
+ * for signals [j0, j0 + n), written contiguously to out: record 0 = block as
+ * float64 (n values), 1 = indices as float64 and 2 = values, each k per signal
+ * (the column-major k x m payload of data.py:232-237).  indices / values are the
+ * device code layout (k rows of stride ld).  Records 3 (energy) and 4
+ * (residual_sq) are the device float64 arrays as they are.
+ */
+int sbo_codes_pack(int record, const int32_t* block, const int16_t* indices, const double* values,
+                   int64_t ld, int k, int64_t j0, int64_t n, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

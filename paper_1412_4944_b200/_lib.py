@@ -64,6 +64,7 @@ _SIGS = {
     "sbo_defect": (I, [P, I, I, P, P]),
     "sbo_frobenius_sq": (I, [P, I, I64, I, P, P, I, I64, P, P, P, P, SZ, P]),
     "sbo_extract_patches": (I, [P, I, I64, I64, I64, I, P, P, I64, I, I, P, P]),
+    "sbo_codes_pack": (I, [I, P, P, P, I64, I, I64, I64, P, P]),
 }
 
 _lib = None

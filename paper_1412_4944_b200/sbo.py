@@ -197,6 +197,29 @@ def represent(y: np.ndarray, dictionary: UnionDictionary, s0: int, kind: str = "
             ThresholdedCode(idx[:, :m].cpu().numpy().astype(np.int64), val[:, :m].cpu().numpy()))
 
 
+def represent_device(y, dictionary: UnionDictionary, s0: int, kind: str = "squared-sum",
+                     chunk_size: int = REPRESENT_TILE, workers: int | None = None):
+    """represent() with the result left on the device: a ``store.DeviceCode`` (for
+    streaming to disk with ``store.save_sbo_codes`` or further device work).  Same
+    validation and values as represent()."""
+    from .store import DeviceCode
+    _check_kind(kind)
+    dictionary.validate()
+    dev = require_device()
+    sig, p, m = _signals(y, dev)
+    if p != dictionary.p:
+        raise ValueError(f"signals have dimension {p}, dictionary blocks {dictionary.p}")
+    if s0 < 1:
+        raise ValueError(f"s0 must be at least 1, got {s0}")
+    if chunk_size < 1:
+        raise ValueError(f"chunk_size must be at least 1, got {chunk_size}")
+    resolve_workers(workers)
+    eng = Engine(sig, s0, kind, k_cap=dictionary.num_blocks)
+    eng.set_blocks(np.stack(dictionary.blocks))
+    best, energy, resid, idx, val = _code_all(eng)
+    return DeviceCode(best, idx, val, energy, resid)
+
+
 def worst_set(assignment: Assignment, w: int) -> np.ndarray:
     """sbo.py:223-228 — the w largest residuals, descending, ties toward low indices."""
     if w < 1:

@@ -211,9 +211,41 @@ def make_ingest():
     np.savez_compressed(HERE / "ingest_patches.npz", **out)
 
 
+def make_store():
+    """store.py:53-133 files (dictionary union + dense, SBO codes), as bytes."""
+    import tempfile
+    from orthodict import store as rstore
+    rng = np.random.default_rng(17)
+    m, k = 37, 5
+    code = rsbo.SparseCode(block=rng.integers(0, 3, m), indices=np.sort(rng.integers(0, 16, (k, m)), axis=0),
+                           values=rng.standard_normal((k, m)), energy=rng.uniform(0, 2, m),
+                           residual_sq=rng.uniform(0, 1, m))
+    union = rsbo.UnionDictionary([_orth(4, rng) for _ in range(3)])
+    dense = rng.standard_normal((6, 9))
+    out = {"block": code.block, "indices": code.indices, "values": code.values,
+           "energy": code.energy, "residual_sq": code.residual_sq,
+           "union": np.stack(union.blocks), "dense": dense}
+    with tempfile.TemporaryDirectory() as t:
+        rstore.save_sbo_codes(t, code)
+        out["codes_odm"] = np.frombuffer((Path(t) / "codes.odm").read_bytes(), np.uint8)
+        out["codes_meta"] = np.array((Path(t) / "codes.meta.json").read_text())
+    with tempfile.TemporaryDirectory() as t:
+        rstore.save_dictionary(t, union, {"note": "x"})
+        out["union_odm"] = np.frombuffer((Path(t) / "dict.odm").read_bytes(), np.uint8)
+        out["union_meta"] = np.array((Path(t) / "dict.meta.json").read_text())
+    with tempfile.TemporaryDirectory() as t:
+        rstore.save_dictionary(t, dense)
+        out["dense_odm"] = np.frombuffer((Path(t) / "dict.odm").read_bytes(), np.uint8)
+        out["dense_meta"] = np.array((Path(t) / "dict.meta.json").read_text())
+    np.savez_compressed(HERE / "store_files.npz", **out)
+
+
 def main():
     if sys.argv[1:] == ["ingest"]:
         make_ingest()
+        return
+    if sys.argv[1:] == ["store"]:
+        make_store()
         return
     u8 = make_patches()
     d, y = make_represent(u8)
@@ -222,6 +254,7 @@ def main():
     make_train(u8)
     make_small()
     make_ingest()
+    make_store()
     (HERE / "VERSIONS.txt").write_text(
         f"orthodict {orthodict.__version__}\nnumpy {np.__version__}\n"
         f"scipy {__import__('scipy').__version__}\n")
