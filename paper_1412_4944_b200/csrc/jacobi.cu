@@ -461,10 +461,17 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
   };
   const double* Pb = P + static_cast<int64_t>(b) * N * N;
   double nrm = 0.0;
-  for (int e = tid; e < N * N; e += kJacobiThreads) {
-    const double v = Pb[e];
-    *at(0, e >> 6, e & 63) = v;
-    nrm = fma(v, v, nrm);
+  {  // all 16 loads in flight before the first store (one global latency, not 16)
+    constexpr int PER = N * N / kJacobiThreads;
+    double v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) v[u] = __ldg(Pb + tid + u * kJacobiThreads);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * kJacobiThreads;
+      *at(0, e >> 6, e & 63) = v[u];
+      nrm = fma(v[u], v[u], nrm);
+    }
   }
   nrm = sqrt(block_sum<kJacobiThreads>(nrm, red));
   if (!(nrm > 0.0)) {

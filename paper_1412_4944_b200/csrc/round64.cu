@@ -103,14 +103,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
   unsigned char* fl = smem + L.flag_off + warp * 64;
   const int seg = blockIdx.x;
   const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
-  if constexpr (MODE != MODE_GRAM) {
-    const int b = block_override >= 0 ? block_override : seg_block[seg];
-    const double* q = blocks + static_cast<int64_t>(b) * p * p;
-    for (int e = tid; e < 64 * 64; e += kThreads) {  // the block, zero padded to 64 x 64
-      const int kk = e >> 6, ii = e & 63;
-      sQ[kk * LD + ii] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
-    }
-  }
   // P accumulator (outer mode), DMMA fragments: warp w owns rows [8w, 8w+8) x 64 atoms
   double acc[8][2];
 #pragma unroll
@@ -146,6 +138,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     }
   };
   if (NB == 2) stage(lo, 0);
+  // (the first tile's copies are in flight while the block is loaded)
+  if constexpr (MODE != MODE_GRAM) {
+    const int b = block_override >= 0 ? block_override : seg_block[seg];
+    const double* q = blocks + static_cast<int64_t>(b) * p * p;
+    // the block, zero padded to 64 x 64: all 16 loads per thread in flight at
+    // once (a load-store loop would pay one L2 latency per element)
+    constexpr int PER = 64 * 64 / kThreads;
+    double v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * kThreads, kk = e >> 6, ii = e & 63;
+      v[u] = (kk < p && ii < p) ? __ldg(q + kk * p + ii) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * kThreads;
+      sQ[(e >> 6) * LD + (e & 63)] = v[u];
+    }
+  }
   int it = 0;
   for (int64_t t0 = lo; t0 < hi; t0 += kTile, ++it) {
     const int buf = NB == 2 ? (it & 1) : 0;
