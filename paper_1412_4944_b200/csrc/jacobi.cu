@@ -439,7 +439,7 @@ __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, ui
 
 __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThreads)
     k_polar_ns_cluster(const double* __restrict__ P, const int64_t* __restrict__ counts,
-                       double* Q, int32_t* status) {
+                       double* Q, int32_t* status, double l0) {
   constexpr int N = 64, NC = kNsCluster, W = N / NC, SL = kNsSliceLd, SZ = kNsSlice;
   constexpr int A2 = W / 8;  // 8-column tiles per slice
   static_assert(W % 8 == 0 && (SL % 16 == 4 || SL % 16 == 12), "slice layout");
@@ -490,7 +490,7 @@ __global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThre
   cluster_barrier();
   constexpr uint32_t kTx = (NC - 1) * SZ * sizeof(double);  // bytes received per iteration
   uint32_t phases = 0u;  // bit u: parity of full[u]
-  double l = 1e-6;
+  double l = l0;
   int it = 0, cur = 0;
   bool done = false;
   for (; it < kNsMaxIter; ++it) {
@@ -1076,8 +1076,17 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
       const size_t nsb = 120 * 1024;
       cudaFuncSetAttribute(k_polar_ns_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(nsb));
+      // Chen-Chow lower bound l0 for sigma_min(P) / ||P||_F: on the benchmark's patch
+      // data the P matrices have ratios ~1e-5 .. 1e-4, where l0 = 1e-5 converges in
+      // 17 iterations (1e-6: 19; 1e-4: 19-20; 1e-3: 23).  A ratio below l0 only
+      // costs iterations (1e-6 with l0 = 1e-5: 23), never accuracy: the stop test
+      // is on ||X^T X - I||.  SBO_NS_L0 overrides it.
+      static const double l0 = [] {
+        const char* e = std::getenv("SBO_NS_L0");
+        return e ? std::atof(e) : 1e-5;
+      }();
       k_polar_ns_cluster<<<K * kNsCluster, kJacobiThreads, nsb, as_stream(stream)>>>(
-          P, counts, Q, status);
+          P, counts, Q, status, l0);
       if (int rc = check_launch("k_polar_ns_cluster")) return rc;
     }
   }
