@@ -102,6 +102,13 @@ int sbo_tc_energy(const void* yh, const void* yl, const int16_t* escale, int64_t
                   const void* qh, const void* ql, const int16_t* fscale, int b0, int b1, int s0,
                   int kind, int accumulate, int32_t* best, double* score, double* residual_sq,
                   int32_t* flags, int32_t* nflag, int32_t* cand, void* stream);
+/* p = 256 (config D), s0 <= 32: the same contract as sbo_tc_energy on operands
+ * from sbo_tc_split_signals / sbo_tc_split_blocks with p = 256 (tc_energy256.cu). */
+int sbo_tc_energy256(const void* yh, const void* yl, const int16_t* escale, int64_t m,
+                     const void* qh, const void* ql, const int16_t* fscale, int b0, int b1,
+                     int s0, int kind, int accumulate, int32_t* best, double* score,
+                     double* residual, int32_t* flags, int32_t* nflag, int32_t* cand,
+                     void* stream);
 
 /* Candidate blocks of the flagged signals (cand, optional, parallel to flags):
  * bit b - b0 set for every block whose approximate decision value was within

@@ -30,6 +30,7 @@ _SIGS = {
     "sbo_tc_split_signals": (I, [P, I, I64, I, P, P, P, P]),
     "sbo_tc_split_blocks": (I, [P, I, I, P, P, P, P]),
     "sbo_tc_energy": (I, [P, P, P, I64, P, P, P, I, I, I, I, I, P, P, P, P, P, P, P]),
+    "sbo_tc_energy256": (I, [P, P, P, I64, P, P, P, I, I, I, I, I, P, P, P, P, P, P, P]),
     "sbo_cand_workspace_bytes": (SZ, []),
     "sbo_cand_sort": (I, [P, P, P, I64, P, P, P, SZ, P]),
     "sbo_energy_recheck_cand": (I, [P, I, I64, I, P, I, I, I, P, P, P, I64, P, P, P, P]),

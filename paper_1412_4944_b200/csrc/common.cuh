@@ -19,6 +19,11 @@ void set_error(const std::string& msg);
 }  // namespace sbo
 
 // round64.cu: Gram partials of a member list on DMMA (p <= 64)
+// p = 256 tensor-core operand preparation (tc_energy256.cu)
+int tc256_split_signals(const void* y, int dtype, int64_t m, int64_t m_pad, void* yh, void* yl,
+                        int16_t* escale, cudaStream_t st);
+int tc256_split_blocks(const double* Q, int K, void* qh, void* ql, int16_t* fscale,
+                       cudaStream_t st);
 int sbo_gram_partials64(const void* y, int dtype, int p, const int32_t* members,
                         const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg,
                         int64_t max_seg, double* partial, void* stream);

@@ -426,7 +426,10 @@ extern "C" int sbo_tc_split_signals(const void* y, int dtype, int64_t m, int p, 
                                     void* ylv, int16_t* escale, void* stream) {
   __half* yh = static_cast<__half*>(yhv);
   __half* yl = static_cast<__half*>(ylv);
-  if (p != tc::P) return fail(SBO_EINVAL, "the tensor-core path needs p = 64");
+  if (p == 256)
+    return tc256_split_signals(y, dtype, m, sbo_tc_padded_rows(m), yhv, ylv, escale,
+                               as_stream(stream));
+  if (p != tc::P) return fail(SBO_EINVAL, "the tensor-core path needs p = 64 or 256");
   const int64_t mp = sbo_tc_padded_rows(m);
   if (mp == 0) return SBO_OK;
   const unsigned grid = static_cast<unsigned>(ceil_div(mp * 32, 256));
@@ -443,7 +446,8 @@ extern "C" int sbo_tc_split_blocks(const double* Q, int K, int p, void* qhv, voi
                                    int16_t* fscale, void* stream) {
   __half* qh = static_cast<__half*>(qhv);
   __half* ql = static_cast<__half*>(qlv);
-  if (p != tc::P) return fail(SBO_EINVAL, "the tensor-core path needs p = 64");
+  if (p == 256) return tc256_split_blocks(Q, K, qhv, qlv, fscale, as_stream(stream));
+  if (p != tc::P) return fail(SBO_EINVAL, "the tensor-core path needs p = 64 or 256");
   if (K < 1) return SBO_OK;
   tc::k_split_blocks<<<K, 256, 0, as_stream(stream)>>>(Q, K, qh, ql, fscale);
   return check_launch("k_split_blocks");

@@ -26,7 +26,7 @@ import torch
 
 from . import _lib as L
 
-SEG_LEN = 1024        # max signals per segment of the per-block kernels
+SEG_LEN = int(os.environ.get("SBO_SEG_LEN", 1024))  # max signals per segment of the per-block kernels
 FILL_CTAS = 2 * 148   # enough segments to fill every SM twice
 
 
@@ -213,11 +213,14 @@ class Engine:
         # representation's residual pass); the incremental re-decision needs them
         self.exact_scores = False
         # tensor-core representation (p = 64): split-fp16 operands, built once
-        self.tc = self.p == 64 and os.environ.get("SBO_TC", "1") != "0" and self.m > 0
+        # tensor-core representation pass: p = 64 (tc_energy.cu) and p = 256 with
+        # s0 <= 32 (tc_energy256.cu); other shapes run the float64 tile kernels
+        self.tc = ((self.p == 64 or (self.p == 256 and min(s0, self.p) <= 32))
+                   and os.environ.get("SBO_TC", "1") != "0" and self.m > 0)
         if self.tc:
             mp = L.size("sbo_tc_padded_rows", self.m)
-            self.yh = torch.zeros((mp, 64), dtype=torch.float16, device=self.dev)
-            self.yl = torch.zeros((mp, 64), dtype=torch.float16, device=self.dev)
+            self.yh = torch.zeros((mp, self.p), dtype=torch.float16, device=self.dev)
+            self.yl = torch.zeros((mp, self.p), dtype=torch.float16, device=self.dev)
             self.escale = torch.zeros(mp, dtype=torch.int16, device=self.dev)
             self.flags = torch.empty(self.m, dtype=torch.int32, device=self.dev)
             self.nflag = torch.zeros(1, dtype=torch.int32, device=self.dev)
@@ -232,8 +235,8 @@ class Engine:
                        self.stream)
 
     def _alloc_tc_blocks(self, cap: int):
-        self.qh = torch.zeros((cap, 64, 64), dtype=torch.float16, device=self.dev)
-        self.ql = torch.zeros((cap, 64, 64), dtype=torch.float16, device=self.dev)
+        self.qh = torch.zeros((cap, self.p, self.p), dtype=torch.float16, device=self.dev)
+        self.ql = torch.zeros((cap, self.p, self.p), dtype=torch.float16, device=self.dev)
         self.fscale = torch.zeros(cap, dtype=torch.int16, device=self.dev)
 
     # ------------------------------------------------------------------ utils
@@ -325,7 +328,8 @@ class Engine:
                 self.cand = torch.empty(self.m, **i32)
                 self.flags_sorted = torch.empty(self.m, **i32)
                 self.cand_sorted = torch.empty(self.m, **i32)
-            self._call("sbo_tc_energy", self.yh.data_ptr(), self.yl.data_ptr(),
+            self._call("sbo_tc_energy" if self.p == 64 else "sbo_tc_energy256",
+                       self.yh.data_ptr(), self.yl.data_ptr(),
                        self.escale.data_ptr(), self.m, self.qh.data_ptr(), self.ql.data_ptr(),
                        self.fscale.data_ptr(), b0, b1, self.s0, self.kind, int(accumulate),
                        s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
