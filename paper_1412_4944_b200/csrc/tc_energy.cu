@@ -95,7 +95,8 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
       sm100::mbar_init(&S->b_full[s], 1);
       sm100::mbar_init(&S->b_empty[s], 1);
       sm100::mbar_init(&S->acc_full[s], 1);
-      sm100::mbar_init(&S->acc_empty[s], EPI_WARPS);
+      // one block: each epilogue group takes alternate tiles (and one stage)
+      sm100::mbar_init(&S->acc_empty[s], nblk == 1 ? EPI_WARPS / 2 : EPI_WARPS);
     }
     sm100::fence_barrier_init();
   }
@@ -179,6 +180,94 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
         if (accumulate) prev_ = ABS ? __ldcg(score + jj) : __ldcg(residual + jj);
       }
     };
+    // one block's decision inputs from its 64 TMEM columns: the signal norm sq,
+    // discarded energy r, kept energy e and decision value dec (unscaled)
+    auto eval_block = [&](uint32_t taddr, int b, int es, float& sq, float& r, float& e,
+                      float& dec) {
+      float v[64];
+      sm100::tmem_ld64(taddr, v);
+      float t8[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = fmaf(v[8 * a + i], v[8 * a + i], acc);
+        t8[a] = acc;
+      }
+      sq = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = ABS ? fabsf(v[i]) : v[i] * v[i];
+      // squared-sum: the discarded energy R is summed from the values the
+      // network drops (+ the tail of the top-G list beyond k): no S - kept cancellation
+      float dropped = 0.0f;
+      if constexpr (ABS) topk::top_of_64<G>(v);
+      else if (ksel == G) dropped = topk::top_of_64_dropped<G, false>(v);  // order unused
+      else dropped = topk::top_of_64_dropped<G>(v);
+      float kept = 0.0f;
+      e = 0.0f;
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if (i < ksel) {
+          kept += ABS ? v[i] * v[i] : v[i];
+          e += v[i];
+        } else if (!ABS) {
+          dropped += v[i];
+        }
+      }
+      // unscale by 2^-(e_s + f_b), exact
+      const float u = exp2f(static_cast<float>(-(es + fscale[b])));
+      const float u2 = u * u;
+      sq *= u2;
+      kept *= u2;
+      e *= ABS ? u : u2;
+      r = ABS ? sq - kept : dropped * u2;
+      dec = ABS ? -e : r;
+    };
+    if (nblk == 1) {
+      // a single block (represent #1's appended block): the two groups take
+      // alternate tiles — accumulator stage g holds this group's tiles — so no
+      // epilogue warp idles and no cross-group combine is needed
+      int es_next;
+      double prev_next;
+      const int64_t tstep = 2 * static_cast<int64_t>(gridDim.x);
+      preload(blockIdx.x + grp * gridDim.x, es_next, prev_next);
+      uint32_t phg = 0;
+      for (int64_t t = blockIdx.x + grp * gridDim.x; t < ntiles; t += tstep) {
+        const int64_t j = t * M + row;
+        const bool valid = j < m;
+        const int es = es_next;
+        const double prev_pre = prev_next;
+        preload(t + tstep, es_next, prev_next);
+        sm100::mbar_wait(&S->acc_full[grp], phg);
+        phg ^= 1u;
+        sm100::tc_fence_after();
+        float sq, r, e, dec;
+        eval_block(lane_base + grp * 256, b0, es, sq, r, e, dec);
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&S->acc_empty[grp]);
+        if (!valid) continue;
+        const float dc = coef_err(sq);
+        const int nd = P - ksel;
+        auto err = [&](float dv) -> float {
+          return ABS ? (ksel * dc + 1e-6f * fabsf(dv)) : resid_err(dv, sq, dc, nd);
+        };
+        if (accumulate) {
+          const float prev = ABS ? -static_cast<float>(prev_pre) : static_cast<float>(prev_pre);
+          const bool flag = fabsf(dec - prev) <= err(dec) + err(prev);
+          if (dec < prev) {
+            best[j] = b0;
+            score[j] = ABS ? e : static_cast<double>(sq) - r;
+            residual[j] = r;
+          }
+          if (flag) flags[atomicAdd(nflag, 1)] = static_cast<int32_t>(j);
+        } else {
+          best[j] = b0;
+          score[j] = ABS ? e : static_cast<double>(sq) - r;
+          residual[j] = r;
+        }
+      }
+    } else {
     int es_next;
     double prev_next;
     preload(blockIdx.x, es_next, prev_next);
@@ -201,43 +290,8 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           const int jb = 2 * grp + h;
           if (jb >= nb) break;
           const int b = b0 + c * CHUNK + jb;
-          float v[64];
-          sm100::tmem_ld64(lane_base + racc.i * 256 + jb * 64, v);
-          float t8[8];
-#pragma unroll
-          for (int a = 0; a < 8; ++a) {
-            float acc = 0.0f;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc = fmaf(v[8 * a + i], v[8 * a + i], acc);
-            t8[a] = acc;
-          }
-          float sq = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
-#pragma unroll
-          for (int i = 0; i < 64; ++i) v[i] = ABS ? fabsf(v[i]) : v[i] * v[i];
-          // squared-sum: the discarded energy R is summed from the values the
-          // network drops (+ the tail of the top-G list beyond k): no S - kept cancellation
-          float dropped = 0.0f;
-          if constexpr (ABS) topk::top_of_64<G>(v);
-          else if (ksel == G) dropped = topk::top_of_64_dropped<G, false>(v);  // order unused
-          else dropped = topk::top_of_64_dropped<G>(v);
-          float kept = 0.0f, e = 0.0f;
-#pragma unroll
-          for (int i = 0; i < G; ++i) {
-            if (i < ksel) {
-              kept += ABS ? v[i] * v[i] : v[i];
-              e += v[i];
-            } else if (!ABS) {
-              dropped += v[i];
-            }
-          }
-          // unscale by 2^-(e_s + f_b), exact
-          const float u = exp2f(static_cast<float>(-(es + fscale[b])));
-          const float u2 = u * u;
-          sq *= u2;
-          kept *= u2;
-          e *= ABS ? u : u2;
-          const float r = ABS ? sq - kept : dropped * u2;
-          const float dec = ABS ? -e : r;
+          float sq, r, e, dec;
+          eval_block(lane_base + racc.i * 256 + jb * 64, b, es, sq, r, e, dec);
           if (dec < d1) {
             d2 = d1;
             d1 = dec;
@@ -321,6 +375,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS));
     }
+    }  // nblk > 1
   }
   __syncthreads();
   if (warp == 2) sm100::tmem_dealloc(tmem, 512);
