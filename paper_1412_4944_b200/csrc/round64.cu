@@ -202,7 +202,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     };
     uint32_t mask = 0u;
     unsigned need;
-    if (k < 16) {
+    if (k <= 8) {
+      // top-8 per lane (two sorted 8s merged), merged across the quad: the k-th
+      // largest fp32 magnitude t_k; the kept set is {|c| >= t_k} when exactly k
+      // magnitudes reach it (no fp32 tie at the threshold) — half the comparators
+      // of the 16-wide network below
+      float srt[8], oth[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        srt[u] = mag(u);
+        oth[u] = mag(u + 8);
+      }
+      topk::sort8_desc(srt);
+      topk::sort8_desc(oth);
+      topk::merge_top<8>(srt, oth);
+#pragma unroll
+      for (int x = 1; x <= 2; x <<= 1) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) oth[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
+        topk::merge_top<8>(srt, oth);
+      }
+      float tk = srt[0];
+#pragma unroll
+      for (int u = 1; u < 8; ++u) tk = select_f(u == k - 1, srt[u], tk);
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (mag(u) >= tk && mag(u) >= 0.0f) {
+          mask |= 1u << u;
+          ++cnt;
+        }
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+      need = __ballot_sync(0xffffffffu, act && cnt != k && t4 == 0);
+    } else if (k < 16) {
       float srt[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) srt[u] = mag(u);
