@@ -6,12 +6,14 @@
 //   tile with mma.sync m8n8k4 f64; the accumulator fragment leaves each quad
 //   of lanes (t4 = lane & 3) holding one signal's 64 coefficients, 16 per lane
 //   (atoms 8n + 2 t4 + h).  Nothing is written back to shared memory.
-// * Selection (select_top, onb.py:58-76): fp32 magnitudes are a monotone
-//   rounding of the float64 ones, so when the k-th and (k+1)-th largest fp32
-//   magnitudes differ the kept set is exactly {i : fp32|c_i| >= t_k} — the
-//   float64 stable-argsort set.  A quad bitonic network finds t_k; a signal
-//   whose fp32 k-th/(k+1)-th magnitudes tie is re-decided by its warp with the
-//   exact rank rule (pick_row).  For k >= 16 every signal takes that path.
+// * Selection (select_top, onb.py:58-76): the high 32 bits of |c| (sign
+//   cleared) are a monotone key of the float64 magnitude, so when exactly k keys
+//   reach the k-th largest key t_k the kept set is {i : key_i >= t_k} — the
+//   float64 stable-argsort set.  Quad networks find t_k (top-8 lists for k <= 8,
+//   top-16 for k < 16, bisection on the key bits for k >= 16); a signal with a
+//   key tie at the threshold (a 2^-20 relative gap) is re-decided by its warp with
+//   the exact rank rule (pick_row).  Keys need no float64 -> float32 conversion:
+//   the XU pipe is left to the signal conversions (it ran at 81 % with them).
 // * Outer product (sparse_outer, onb.py:127-134): the kept values are written as
 //   a dense X tile (zeros elsewhere) and P += Y^T X runs on DMMA in signal order
 //   (deterministic partials, no atomics).  A sparse DFMA form (2 p k flop per
@@ -71,6 +73,14 @@ __device__ __forceinline__ float select_f(bool c, float a, float b) {
   asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}"
       : "=f"(r)
       : "f"(a), "f"(b), "r"(static_cast<int>(c)));
+  return r;
+}
+
+__device__ __forceinline__ int select_i(bool c, int a, int b) {
+  int r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+      : "=r"(r)
+      : "r"(a), "r"(b), "r"(static_cast<int>(c)));
   return r;
 }
 
@@ -197,21 +207,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     // exact selection in registers
     const bool act = rows[s] >= 0;
     // magnitudes are recomputed from c where needed (register pressure)
-    auto mag = [&](int u) -> float {
-      return (act && atom_of(u, t4) < p) ? static_cast<float>(fabs(c[u >> 1][u & 1])) : -1.0f;
+    // selection keys: the high word of |c| (sign cleared) orders like |c| — no
+    // float64 -> float32 conversion (the XU pipe the Y conversions already load);
+    // 20 mantissa bits, so a key tie (re-decided exactly) is a 2^-20 relative gap.
+    // -1: inactive signal or atom beyond p.
+    auto key = [&](int u) -> int {
+      return (act && atom_of(u, t4) < p) ? (__double2hiint(c[u >> 1][u & 1]) & 0x7FFFFFFF) : -1;
     };
     uint32_t mask = 0u;
     unsigned need;
     if (k <= 8) {
-      // top-8 per lane (two sorted 8s merged), merged across the quad: the k-th
-      // largest fp32 magnitude t_k; the kept set is {|c| >= t_k} when exactly k
-      // magnitudes reach it (no fp32 tie at the threshold) — half the comparators
-      // of the 16-wide network below
-      float srt[8], oth[8];
+      // top-8 keys per lane (two sorted 8s merged), merged across the quad: the
+      // k-th largest key t_k; the kept set is {key >= t_k} when exactly k keys
+      // reach it (no tie at the threshold) — half the comparators of the 16-wide
+      // network below
+      int srt[8], oth[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        srt[u] = mag(u);
-        oth[u] = mag(u + 8);
+        srt[u] = key(u);
+        oth[u] = key(u + 8);
       }
       topk::sort8_desc(srt);
       topk::sort8_desc(oth);
@@ -222,13 +236,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
         for (int u = 0; u < 8; ++u) oth[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
         topk::merge_top<8>(srt, oth);
       }
-      float tk = srt[0];
+      int tk = srt[0];
 #pragma unroll
-      for (int u = 1; u < 8; ++u) tk = select_f(u == k - 1, srt[u], tk);
+      for (int u = 1; u < 8; ++u) tk = select_i(u == k - 1, srt[u], tk);
       int cnt = 0;
 #pragma unroll
       for (int u = 0; u < 16; ++u)
-        if (mag(u) >= tk && mag(u) >= 0.0f) {
+        if (key(u) >= tk && key(u) >= 0) {
           mask |= 1u << u;
           ++cnt;
         }
@@ -236,38 +250,38 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
       need = __ballot_sync(0xffffffffu, act && cnt != k && t4 == 0);
     } else if (k < 16) {
-      float srt[16];
+      int srt[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) srt[u] = mag(u);
+      for (int u = 0; u < 16; ++u) srt[u] = key(u);
       topk::sort_desc<16>(srt);
 #pragma unroll
       for (int x = 1; x <= 2; x <<= 1) {
-        float other[16];
+        int other[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) other[u] = __shfl_xor_sync(0xffffffffu, srt[u], x);
         topk::merge_top<16>(srt, other);
       }
       // the k-th / (k+1)-th largest by register selects (a plain srt[k - 1] with
       // runtime k would go through local memory)
-      float tk = srt[0], tk1 = srt[1];
+      int tk = srt[0], tk1 = srt[1];
 #pragma unroll
       for (int u = 1; u < 16; ++u) {
-        tk = select_f(u == k - 1, srt[u], tk);
-        tk1 = select_f(u == k, srt[u], tk1);
+        tk = select_i(u == k - 1, srt[u], tk);
+        tk1 = select_i(u == k, srt[u], tk1);
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u)
-        if (mag(u) >= tk && mag(u) >= 0.0f) mask |= 1u << u;
-      // float32 ties at the threshold: the warp re-decides those signals exactly
+        if (key(u) >= tk && key(u) >= 0) mask |= 1u << u;
+      // key ties at the threshold: the warp re-decides those signals exactly
       need = __ballot_sync(0xffffffffu, act && !(tk > tk1) && t4 == 0);
     } else {
-      // k >= 16: the k-th largest fp32 magnitude of the quad's 64 by bisection on
-      // its bit pattern (non-negative floats order like their bits): the largest T
+      // k >= 16: the k-th largest key of the quad's 64 by bisection on its bits:
+      // the largest T
       // with #{|c| >= T} >= k.  Exactly k at or above T: the kept set; otherwise a
       // tie at the threshold, re-decided by the warp's exact rank rule.
-      uint32_t key[16];
+      uint32_t ukey[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) key[u] = mag(u) >= 0.0f ? __float_as_uint(mag(u)) : 0u;
+      for (int u = 0; u < 16; ++u) ukey[u] = key(u) >= 0 ? static_cast<uint32_t>(key(u)) : 0u;
       const uint32_t vmask = [&] {
         uint32_t v = 0u;
 #pragma unroll
@@ -280,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
         const uint32_t cand = T | (1u << bit);
         int cnt = 0;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) cnt += ((vmask >> u) & 1u) && key[u] >= cand;
+        for (int u = 0; u < 16; ++u) cnt += ((vmask >> u) & 1u) && ukey[u] >= cand;
         cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
         cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
         if (cnt >= k) T = cand;
@@ -288,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       int cnt = 0;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const bool on = ((vmask >> u) & 1u) && key[u] >= T;
+        const bool on = ((vmask >> u) & 1u) && ukey[u] >= T;
         cnt += on;
         if (on) mask |= 1u << u;
       }
@@ -327,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       for (int u = 0; u < 16; ++u) {
         const double v = c[u >> 1][u & 1];
         if ((mask >> u) & 1u) e = kind == SBO_KIND_SQUARED_SUM ? fma(v, v, e) : e + fabs(v);
-        else if (mag(u) >= 0.0f) d = fma(v, v, d);
+        else if (act && atom_of(u, t4) < p) d = fma(v, v, d);
       }
       d += __shfl_xor_sync(0xffffffffu, d, 1);
       d += __shfl_xor_sync(0xffffffffu, d, 2);

@@ -6,16 +6,23 @@
 namespace sbo {
 namespace topk {
 
+// element max / min: FMNMX for float32 values, IMNMX for integer keys
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ int vmax(int a, int b) { return max(a, b); }
+__device__ __forceinline__ int vmin(int a, int b) { return min(a, b); }
+
 // compare-exchange so that v[i] >= v[j]
-__device__ __forceinline__ void cx(float& a, float& b) {
-  const float hi = fmaxf(a, b), lo = fminf(a, b);
+template <typename T>
+__device__ __forceinline__ void cx(T& a, T& b) {
+  const T hi = vmax(a, b), lo = vmin(a, b);
   a = hi;
   b = lo;
 }
 
 // a bitonic sequence of N -> sorted descending
-template <int N>
-__device__ __forceinline__ void merge_desc(float* v) {
+template <int N, typename T>
+__device__ __forceinline__ void merge_desc(T* v) {
 #pragma unroll
   for (int half = N / 2; half >= 1; half >>= 1) {
 #pragma unroll
@@ -26,7 +33,8 @@ __device__ __forceinline__ void merge_desc(float* v) {
 }
 
 // 8 values -> sorted descending with the optimal 19-comparator network (depth 6)
-__device__ __forceinline__ void sort8_desc(float* v) {
+template <typename T>
+__device__ __forceinline__ void sort8_desc(T* v) {
   cx(v[0], v[2]); cx(v[1], v[3]); cx(v[4], v[6]); cx(v[5], v[7]);
   cx(v[0], v[4]); cx(v[1], v[5]); cx(v[2], v[6]); cx(v[3], v[7]);
   cx(v[0], v[1]); cx(v[2], v[3]); cx(v[4], v[5]); cx(v[6], v[7]);
@@ -36,8 +44,8 @@ __device__ __forceinline__ void sort8_desc(float* v) {
 }
 
 // any N (power of two) -> sorted descending (bitonic sort; 8 uses sort8_desc)
-template <int N>
-__device__ __forceinline__ void sort_desc(float* v) {
+template <int N, typename T>
+__device__ __forceinline__ void sort_desc(T* v) {
   if constexpr (N == 8) {
     sort8_desc(v);
     return;
@@ -63,10 +71,10 @@ __device__ __forceinline__ void sort_desc(float* v) {
 
 // top-G (sorted descending) of the union of two sorted-descending lists a, b;
 // result in a.  c_i = max(a_i, b_{G-1-i}) is bitonic and holds the top G.
-template <int G>
-__device__ __forceinline__ void merge_top(float* a, const float* b) {
+template <int G, typename T>
+__device__ __forceinline__ void merge_top(T* a, const T* b) {
 #pragma unroll
-  for (int i = 0; i < G; ++i) a[i] = fmaxf(a[i], b[G - 1 - i]);
+  for (int i = 0; i < G; ++i) a[i] = vmax(a[i], b[G - 1 - i]);
   merge_desc<G>(a);
 }
 
