@@ -316,8 +316,11 @@ class Engine:
             # the signals whose certificate failed (near-ties)
             if self.qh.shape[0] < self.k_cap:
                 self._alloc_tc_blocks(self.k_cap)
-            self._call("sbo_tc_split_blocks", self.blocks.data_ptr(), b1, self.p,
-                       self.qh.data_ptr(), self.ql.data_ptr(), self.fscale.data_ptr(),
+            # operands of the blocks this pass reads, [b0, b1)
+            pp = self.p * self.p
+            self._call("sbo_tc_split_blocks", self.blocks.data_ptr() + 8 * b0 * pp, b1 - b0,
+                       self.p, self.qh.data_ptr() + 2 * b0 * pp,
+                       self.ql.data_ptr() + 2 * b0 * pp, self.fscale.data_ptr() + 2 * b0,
                        self.stream)
             self.nflag.zero_()
             # full pass over <= 32 blocks: the flagged signals carry candidate-block
