@@ -103,7 +103,7 @@ def extract_patches_device(grid, cfg: PatchConfig, device=None, dtype=torch.floa
     grid = _check_grid(grid, e)
     if e * e > 1024:
         raise ValueError(f"patch_edge {e} exceeds the device ingestion limit of 32")
-    dev = require_device() if device is None else torch.device(device)
+    dev = require_device(None if device is None else torch.device(device).index)
     h, w = grid.shape
     if max(h, w) >= 2 ** 31:
         raise ValueError("grid dimensions must be below 2^31")
