@@ -35,7 +35,7 @@ METRIC = "signals/sec per SBO iteration (p=64,K=16,s0=8) at 1/2/4/8 B200 vs CPU 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--m-per-gpu", dest="m", type=int, default=1 << 20, help="signals per GPU")
