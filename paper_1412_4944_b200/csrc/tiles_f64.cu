@@ -92,14 +92,28 @@ __device__ void project_tile_dmma(const TY* __restrict__ y, int p, const int64_t
     for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
     for (int kc = 0; kc < p; kc += 64) {
       __syncthreads();
-      for (int e = tid; e < kTile * 64; e += kThreads) {
-        const int s = e >> 6, kk = e & 63;
-        const int64_t r = rows[s];
-        sY[s * kDmmaLd + kk] =
-            (r >= 0 && kc + kk < p) ? static_cast<double>(__ldg(y + r * p + kc + kk)) : 0.0;
-        sQ[s * kDmmaLd + kk] = (kc + s < p && ic + kk < p)
-                                   ? __ldg(q + static_cast<int64_t>(kc + s) * p + ic + kk)
-                                   : 0.0;
+      // the chunk's loads in batches of 8 per thread, all in flight before the
+      // batch's stores (a load-store loop pays one memory latency per element,
+      // 16 of them per chunk and 16 chunks per tile at p = 256)
+      constexpr int PER = kTile * 64 / kThreads, BATCH = 8;
+#pragma unroll
+      for (int u0 = 0; u0 < PER; u0 += BATCH) {
+        double vy[BATCH], vq[BATCH];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int e = tid + (u0 + u) * kThreads, s = e >> 6, kk = e & 63;
+          const int64_t r = rows[s];
+          vy[u] = (r >= 0 && kc + kk < p) ? static_cast<double>(__ldg(y + r * p + kc + kk)) : 0.0;
+          vq[u] = (kc + s < p && ic + kk < p)
+                      ? __ldg(q + static_cast<int64_t>(kc + s) * p + ic + kk)
+                      : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int e = tid + (u0 + u) * kThreads, s = e >> 6, kk = e & 63;
+          sY[s * kDmmaLd + kk] = vy[u];
+          sQ[s * kDmmaLd + kk] = vq[u];
+        }
       }
       __syncthreads();
       const double* ya = sY + (8 * warp + g) * kDmmaLd + t4;
