@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
   double* sYt = reinterpret_cast<double*>(smem + L.yt_off);  // [s][kk]
   double* sX = reinterpret_cast<double*>(smem + L.x_off);    // [s][ii]
   int64_t* rows = reinterpret_cast<int64_t*>(smem + L.rows_off);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int seg = blockIdx.x;
   const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
   double* out = partial + static_cast<int64_t>(seg) * p * p;
@@ -452,11 +452,11 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
     const int kn = min(64, p - kc);
     for (int ic = 0; ic < p; ic += 64) {
       const int in = min(64, p - ic);
-      double acc[4][4];
+      // P[kc + 8 warp + g][ic + 8 n + 2 t4 + h] on DMMA (m8n8k4): A = Y^T (rows kk,
+      // k = signals), B = X (signals x atoms), signals in order 4 at a time
+      double acc[8][2];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
       for (int64_t t0 = lo; t0 < hi; t0 += kTile) {
         __syncthreads();
         if (tid < kTile) {
@@ -486,26 +486,24 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
           }
         }
         __syncthreads();
-        const int ns = static_cast<int>(min64(kTile, hi - t0));
-        for (int s = 0; s < ns; ++s) {
-          const double2 y01 = *reinterpret_cast<const double2*>(sYt + s * kSyLd + 4 * ty);
-          const double2 y23 = *reinterpret_cast<const double2*>(sYt + s * kSyLd + 4 * ty + 2);
-          const double2 x01 = *reinterpret_cast<const double2*>(sX + s * kSyLd + 4 * tx);
-          const double2 x23 = *reinterpret_cast<const double2*>(sX + s * kSyLd + 4 * tx + 2);
-          const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
-          const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+        // rows of signals beyond the segment are zero in both staged operands
+        const double* ya = sYt + t4 * kSyLd + 8 * warp + g;
+        const double* xb = sX + t4 * kSyLd + g;
+#pragma unroll 4
+        for (int s4 = 0; s4 < kTile; s4 += 4) {
+          const double av = ya[s4 * kSyLd];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(yv[a], xv[b], acc[a][b]);
+          for (int n = 0; n < 8; ++n) dmma8(acc[n][0], acc[n][1], av, xb[s4 * kSyLd + 8 * n]);
         }
       }
+      const int row = 8 * warp + g;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int n = 0; n < 8; ++n)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (4 * ty + a < kn && 4 * tx + b < in)
-            out[static_cast<int64_t>(kc + 4 * ty + a) * p + ic + 4 * tx + b] = acc[a][b];
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * n + 2 * t4 + h;
+          if (row < kn && col < in) out[static_cast<int64_t>(kc + row) * p + ic + col] = acc[n][h];
+        }
     }
   }
 }
