@@ -448,9 +448,12 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
   const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
   double* out = partial + static_cast<int64_t>(seg) * p * p;
 
-  for (int kc = 0; kc < p; kc += 64) {
+  // one 64 x 64 output tile (kc, ic) of the segment's partial per CTA (blockIdx.y)
+  const int nic = (p + 63) / 64;
+  {
+    const int kc = 64 * (static_cast<int>(blockIdx.y) / nic), ic = 64 * (static_cast<int>(blockIdx.y) % nic);
     const int kn = min(64, p - kc);
-    for (int ic = 0; ic < p; ic += 64) {
+    {
       const int in = min(64, p - ic);
       // P[kc + 8 warp + g][ic + 8 n + 2 t4 + h] on DMMA (m8n8k4): A = Y^T (rows kk,
       // k = signals), B = X (signals x atoms), signals in order 4 at a time
@@ -631,7 +634,8 @@ int outer_impl(const void* yv, int p, const int32_t* order, const int64_t* seg_l
   const OuterLayout L;
   cudaFuncSetAttribute(k_outer_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
-  k_outer_f64<TY><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
+  const unsigned nt = static_cast<unsigned>((p + 63) / 64);
+  k_outer_f64<TY><<<dim3(static_cast<unsigned>(max_seg), nt * nt), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), p, order, seg_lo, seg_hi, nseg, k, ld, idx, val, dense_self,
       partial);
   return check_launch("k_outer_f64");
