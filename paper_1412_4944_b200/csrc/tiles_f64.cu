@@ -526,30 +526,42 @@ __global__ void __launch_bounds__(256) k_reduce_segments(const double* __restric
   const int64_t pp = static_cast<int64_t>(p) * p;
   const int el = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int64_t e = static_cast<int64_t>(blockIdx.x) * 32 + el;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // segments are sorted by block: block b's range [s0, s1) by a 32-way search
+    // (each round narrows [lo, hi) to one of 32 slices with one load per lane:
+    // two or three dependent loads instead of a binary search's ~11)
+    const int lane32 = threadIdx.x;
     const int n = *nseg;
-    // segments are sorted by block: binary-search block b's range [s0, s1)
     int s0 = 0, s1 = n;
     if (seg_block) {
-      int a = 0, z = n;
-      while (a < z) {
-        const int mid = (a + z) >> 1;
-        if (seg_block[mid] < b) a = mid + 1;
-        else z = mid;
+      for (int pass = 0; pass < 2; ++pass) {  // pass 0: first s with block >= b; 1: > b
+        const int key = b + pass;
+        int lo = 0, hi = n;  // answer in [lo, hi]
+        while (hi - lo > 0) {
+          const int step = (hi - lo + 31) / 32;
+          const int probe = lo + lane32 * step;
+          const bool below = probe < hi && seg_block[probe] < key;
+          const unsigned bal = __ballot_sync(0xffffffffu, below);
+          const int cnt = __popc(bal);  // probes below key: a prefix of the lanes
+          const int nlo = cnt == 0 ? lo : lo + (cnt - 1) * step + 1;
+          const int nhi = cnt == 0 ? lo : min(hi, lo + cnt * step);
+          if (step == 1) {
+            lo = hi = lo + cnt;
+            break;
+          }
+          lo = nlo;
+          hi = nhi;
+        }
+        if (pass == 0) s0 = lo;
+        else s1 = lo;
       }
-      s0 = a;
-      z = n;
-      while (a < z) {
-        const int mid = (a + z) >> 1;
-        if (seg_block[mid] <= b) a = mid + 1;
-        else z = mid;
-      }
-      s1 = a;
     } else if (b != 0) {
       s1 = 0;
     }
-    range[0] = s0;
-    range[1] = s1;
+    if (lane32 == 0) {
+      range[0] = s0;
+      range[1] = s1;
+    }
   }
   __syncthreads();
   const int s0 = range[0], s1 = range[1];
