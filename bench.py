@@ -4,11 +4,17 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 A step is one ``sbo_train`` loop-body iteration (sbo.py:352-397) entering with
-K-1 = 15 blocks and leaving with K = 16, over m = 2^20 synthetic 8x8 image
-patches per GPU (BASELINE.json config B; weak scaling across ranks, signals
-sharded by contiguous columns).  Every step restores the same entering state.
-Prints ONE JSON line on rank 0.  ``--impl reference`` times the reference
-algorithm on the host cores instead (the CPU oracle port; rank 0 only).
+K-1 = 15 blocks and leaving with K = 16, over m = 2^24 synthetic 8x8 image
+patches of a 4096^2 scene (BASELINE.json config C), sharded by contiguous
+columns over the N GPUs (strong scaling: m/N signals per GPU).  Every step
+restores the same entering state.  Prints ONE JSON line on rank 0.
+
+``--gpus N`` with N > 1 outside torchrun re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL); with
+SBO_BENCH_ONE_GPU=1 every rank shares cuda:0 over gloo (a functional check of
+the sharded path on a one-GPU box, not a performance configuration).
+``--impl reference`` times the reference algorithm on the host cores instead
+(the CPU oracle port on a 2^20-signal sample of the workload; rank 0 only).
 """
 from __future__ import annotations
 
@@ -38,31 +44,67 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--m-per-gpu", dest="m", type=int, default=1 << 20, help="signals per GPU")
+    ap.add_argument("--m", dest="m_total", type=int, default=1 << 24,
+                    help="signals in the whole job (config C: 2^24)")
+    ap.add_argument("--m-per-gpu", dest="m_per_gpu", type=int, default=None,
+                    help="weak scaling: signals per GPU (overrides --m)")
     ap.add_argument("--p-edge", type=int, default=8)
     ap.add_argument("--K", type=int, default=16)
     ap.add_argument("--s0", type=int, default=8)
     ap.add_argument("--rounds", type=int, default=6)
-    ap.add_argument("--scene", type=int, default=2048)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 17)
+    ap.add_argument("--scene", type=int, default=4096)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 20)
+    ap.add_argument("--cpu-steps", type=int, default=3,
+                    help="timed CPU iterations (each one a --cpu-sample iteration)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.m_per_gpu is not None:
+        a.scaling, a.m_total = "weak", a.m_per_gpu * max(a.world, 1)
+    else:
+        a.scaling = "strong"
+    return a
+
+
+def config_label(a):
+    std = {(64, 16, 8, 1 << 24): "C", (64, 16, 8, 1 << 20): "B", (256, 32, 16, 1 << 22): "D"}
+    key = (a.p_edge ** 2, a.K, a.s0, a.m_total)
+    return std.get(key, "E" if (a.p_edge == 8 and a.m_total == 1 << 22) else "custom")
 
 
 def workload_name(a, world):
-    return (f"B: p={a.p_edge**2}, K={a.K} (entering {a.K - 1}), s0={a.s0}, R={a.rounds}, "
-            f"m=2^{int(math.log2(a.m))} per GPU x {world}, W=m/16, {a.p_edge}x{a.p_edge} patches of a "
-            f"{a.scene}^2 synthetic scene")
+    return (f"{config_label(a)}: p={a.p_edge**2}, K={a.K} (entering {a.K - 1}), s0={a.s0}, "
+            f"R={a.rounds}, m=2^{math.log2(a.m_total):g} total over {world} GPU(s) "
+            f"({a.scaling} scaling, {a.m_total // world} per GPU), W=m/16, "
+            f"{a.p_edge}x{a.p_edge} patches of a {a.scene}^2 synthetic scene")
+
+
+def shard_range(a, rank, world):
+    """Contiguous column shard [lo, hi) of rank (the first m % world ranks get one more)."""
+    base, extra = divmod(a.m_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
 
 
 def shard_signals(a, rank, world):
     from paper_1412_4944_b200 import signals
-    m_total = a.m * world
     grid = signals.scene(a.scene, a.scene, 0)
-    u8 = signals.patch_bytes(grid, a.p_edge, m_total, 11)
-    lo, hi = rank * a.m, (rank + 1) * a.m
-    return signals.unit_range(u8[lo:hi]), m_total
+    lo, hi = shard_range(a, rank, world)
+    u8 = signals.patch_bytes(grid, a.p_edge, a.m_total, 11, lo, hi)
+    return signals.unit_range(u8), a.m_total
+
+
+def relaunch_distributed(a):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 class ClockSampler:
@@ -211,20 +253,41 @@ def iteration_model(p, K, s0, R, w_frac):
 
 
 # --------------------------------------------------------------------------- CPU
-def cpu_iteration_sample(a, y_rows, blocks, workers):
-    """Time the reference algorithm (oracle port) on a bounded sample of the workload."""
+def cpu_iteration_sample(a, y_rows, blocks, workers, iters=1, warm=1):
+    """Time the reference algorithm (oracle port) on a bounded sample of the workload:
+    mean seconds of ``iters`` iterations after ``warm`` untimed iterations."""
     from oracle import sbo_oracle as O
     y = y_rows.T.astype(np.float64)
     p, m = y.shape
     rep0 = O.code_signals(y, blocks, a.s0, workers=workers)
     w = max(p, m // 16)
-    t0 = time.perf_counter()
-    O.iterate(y, blocks, rep0.residual_sq, a.s0, a.rounds, w, seed=1, workers=workers)
-    return time.perf_counter() - t0
+    times = []
+    for i in range(iters + warm):
+        t0 = time.perf_counter()
+        O.iterate(y, blocks, rep0.residual_sq, a.s0, a.rounds, w, seed=1, workers=workers)
+        if i >= warm:
+            times.append(time.perf_counter() - t0)
+    return float(np.mean(times))
+
+
+def cpu_sample_note(a, n, workers, t):
+    """The cpu_baseline description, with the linear extrapolation to the full job."""
+    return {"sample": (f"one iteration on the first {n} signals of the workload (p={a.p_edge**2}, "
+                       f"K={a.K - 1}->{a.K}, s0={a.s0}, R={a.rounds}, W=m/16), oracle port: "
+                       f"numpy/OpenBLAS 1 thread + a {workers}-thread pool, same entering "
+                       "blocks"),
+            "extrapolated_s_per_iteration_at_m_total": t * a.m_total / n,
+            "extrapolation": (f"linear in m from the {n}-signal sample to m={a.m_total} "
+                              "(SURVEY.md 8(d)); the CPU per-signal rate falls as m grows "
+                              "(SURVEY.md 3.5), so this favours the CPU")}
 
 
 def run_reference(a):
-    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    """--impl reference: the reference algorithm on the host cores (rank 0 only).
+
+    Each step is one iteration over a --cpu-sample (2^20) sample of the workload;
+    the timed count is min(--steps, --cpu-steps) after min(--warmup, 1) warm-up
+    iterations, so the arm ends within a few minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -232,31 +295,31 @@ def run_reference(a):
     from paper_1412_4944_b200 import signals
     workers = os.cpu_count() or 1
     grid = signals.scene(a.scene, a.scene, 0)
-    rows = signals.unit_range(signals.patch_bytes(grid, a.p_edge, a.cpu_sample, 11))
+    n = min(a.cpu_sample, a.m_total)
+    rows = signals.unit_range(signals.patch_bytes(grid, a.p_edge, a.m_total, 11, 0, n))
     y = rows.T.astype(np.float64)
     p, m = y.shape
     blocks = O.initial_blocks(y, a.s0, a.K - 1, 4096, a.rounds, seed=1, workers=workers)
     rep0 = O.code_signals(y, blocks, a.s0, workers=workers)
     w = max(p, m // 16)
+    steps, warm = max(1, min(a.steps, a.cpu_steps)), min(a.warmup, 1)
     times = []
-    for i in range(a.warmup + a.steps):
+    for i in range(warm + steps):
         t0 = time.perf_counter()
         O.iterate(y, blocks, rep0.residual_sq, a.s0, a.rounds, w, seed=1, workers=workers)
-        if i >= a.warmup:
+        if i >= warm:
             times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
     v = m / t
-    sample = (f"one iteration on the first {m} signals of the same workload (p={p}, "
-              f"K={a.K - 1}->{a.K}, s0={a.s0}, R={a.rounds}, W=m/16); numpy/OpenBLAS, "
-              f"OPENBLAS_NUM_THREADS=1, thread pool of {workers}")
+    cpu = {"value": v, "unit": "signals/s", "cores": workers, "kind": "port"}
+    cpu.update(cpu_sample_note(a, m, workers, t))
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": "signals/s", "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
+        "steps_timed": steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
         "config": {"workload": workload_name(a, a.gpus), "sample_m": m},
-        "cpu_baseline": {"value": v, "unit": "signals/s", "cores": workers, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "signals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -307,10 +370,10 @@ def run_ours(a):
     rows, m_total = shard_signals(a, rank, world)
     p = rows.shape[1]
     eng = Engine(Signals.from_rows(rows, dev), a.s0, k_cap=a.K, comm=comm, m_total=m_total)
-    lo = rank * a.m
+    lo, hi = shard_range(a, rank, world)
 
     def local_cols(cols):
-        sel = cols[(cols >= lo) & (cols < lo + a.m)]
+        sel = cols[(cols >= lo) & (cols < hi)]
         return sel - lo
 
     cfg = SboConfig(s0=a.s0, k0=a.K - 1, p0=4096, rounds=a.rounds, k_max=a.K, seed=1)
@@ -403,7 +466,8 @@ def run_ours(a):
     for v in kernels.values():
         v["ms_per_step"] = v["ms_total"] / a.steps
     f_sig, b_sig = iteration_model(p, a.K, a.s0, a.rounds, 1.0 / 16)
-    t_roof = max(f_sig * a.m / (bf16 / 2 * 1e12), b_sig * a.m / (hbm * 1e9))
+    m_gpu = hi - lo  # the largest shard is rank 0's
+    t_roof = max(f_sig * m_gpu / (bf16 / 2 * 1e12), b_sig * m_gpu / (hbm * 1e9))
     phases = np.mean([[mk.ev[i].elapsed_time(mk.ev[i + 1]) for i in range(4)] for mk in marks],
                      axis=0)
 
@@ -419,11 +483,9 @@ def run_ours(a):
         workers = os.cpu_count() or 1
         n = min(a.cpu_sample, rows.shape[0])
         blocks = [q for q in snap_blocks[:K0].cpu().numpy()]
-        t = cpu_iteration_sample(a, rows[:n], blocks, workers)
-        cpu = {"value": n / t, "unit": "signals/s", "cores": workers, "kind": "port",
-               "sample": f"one iteration on the first {n} signals of the workload, oracle port "
-                         f"(numpy/OpenBLAS 1 thread + {workers}-thread pool), same entering "
-                         f"blocks"}
+        t = cpu_iteration_sample(a, rows[:n], blocks, workers, warm=0)
+        cpu = {"value": n / t, "unit": "signals/s", "cores": workers, "kind": "port"}
+        cpu.update(cpu_sample_note(a, n, workers, t))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -431,11 +493,13 @@ def run_ours(a):
     line = {
         "metric": METRIC, "value": value, "unit": "signals/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded procedural scene, 8x8 patches, float32 signals)",
         "config": {"workload": workload_name(a, world), "p": p, "K": a.K, "s0": a.s0,
-                   "rounds": a.rounds, "m_per_gpu": a.m, "W": w,
-                   "l2": "inputs larger than L2 (fp32 signals 4*p*m bytes per GPU, 256 MB at m=2^20 > 126 MB L2)",
+                   "rounds": a.rounds, "m_total": m_total, "m_per_gpu": hi - lo, "W": w,
+                   "scaling": a.scaling,
+                   "l2": (f"inputs larger than L2 (fp32 signals {4 * p * (hi - lo) / 1e9:.2f} GB "
+                          "per GPU > 126 MB L2)"),
                    "parallelism": f"column shards over {world} GPU(s), NCCL allreduce"},
         "clocks": clocks,
         "gpu_launches": launches,
@@ -461,8 +525,8 @@ def shard_corners(a, rank, world):
     """This rank's patch corners (data.py:199-201 draws over the whole workload)."""
     from paper_1412_4944_b200 import data, signals
     grid = signals.scene(a.scene, a.scene, 0)
-    r, c = data.patch_corners(a.scene, a.scene, a.p_edge, a.m * world, 11)
-    lo, hi = rank * a.m, (rank + 1) * a.m
+    r, c = data.patch_corners(a.scene, a.scene, a.p_edge, a.m_total, 11)
+    lo, hi = shard_range(a, rank, world)
     return grid, r[lo:hi].astype(np.int32), c[lo:hi].astype(np.int32)
 
 
@@ -613,7 +677,11 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
     out = {"value": m_total / t, "unit": "signals/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h,
            "pipelining": "step i+1's input and state uploads overlap step i (copy stream); "
-                         "results leave through a device staging copy on a third stream"}
+                         "results leave through a device staging copy on a third stream",
+           "api": ("the sbo_train loop body through Engine (restore entering state, "
+                   "iterate_device, finish_iteration) with host buffers; the new dictionary, "
+                   "assignment and residuals are read back (codes and energies stay on the "
+                   "device), not the sbo_train/represent entry points themselves")}
     if ingest is not None:
         out["input"] = ("8-bit scene + int32 patch corners per step; patches extracted on the "
                         "device (paper_1412_4944_b200.data, data.py:182-208)")
@@ -622,6 +690,8 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
 
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(a)
     if a.impl == "reference":
         run_reference(a)
     else:

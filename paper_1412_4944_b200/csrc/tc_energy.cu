@@ -74,6 +74,12 @@ __device__ __forceinline__ float resid_err(float r, float s, float d, int n) {
   return 2.0f * d * sqrtf(static_cast<float>(n) * fmaxf(r, 0.0f)) + n * d * d + 8e-6f * fmaxf(r, 0.0f);
 }
 
+// candidate mask of a signal flagged by an incremental pass over [b0, b1)
+// (b1 <= 32): its incoming winner and every appended block
+__device__ __forceinline__ uint32_t accum_cand(int prev, int b0, int b1) {
+  return (prev >= 0 && prev < 32 ? 1u << prev : 0u) | (((1u << (b1 - b0)) - 1u) << b0);
+}
+
 template <int G, bool ABS>
 __global__ void __launch_bounds__(THREADS, 1)
 k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
@@ -255,12 +261,18 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
         if (accumulate) {
           const float prev = ABS ? -static_cast<float>(prev_pre) : static_cast<float>(prev_pre);
           const bool flag = fabsf(dec - prev) <= err(dec) + err(prev);
-          if (dec < prev) {
+          // a flagged signal keeps its incoming exact winner / score: the float64
+          // re-decision compares the new block against them (first maximum wins)
+          if (dec < prev && !flag) {
             best[j] = b0;
             score[j] = ABS ? e : static_cast<double>(sq) - r;
             residual[j] = r;
           }
-          if (flag) flags[atomicAdd(nflag, 1)] = static_cast<int32_t>(j);
+          if (flag) {
+            const int ix = atomicAdd(nflag, 1);
+            flags[ix] = static_cast<int32_t>(j);
+            if (cand) cand[ix] = static_cast<int32_t>(accum_cand(__ldcg(best + j), b0, b1));
+          }
         } else {
           best[j] = b0;
           score[j] = ABS ? e : static_cast<double>(sq) - r;
@@ -343,7 +355,8 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
         if (accumulate) {  // incoming winner covers blocks < b0 and keeps ties
           const float prev = ABS ? -static_cast<float>(prev_pre) : static_cast<float>(prev_pre);
           flag = fabsf(d1 - prev) <= err(d1) + err(prev);
-          if (d1 < prev) {
+          // flagged: keep the incoming exact winner / score for the float64 re-decision
+          if (d1 < prev && !flag) {
             best[j] = bb;
             score[j] = ABS ? eb : static_cast<double>(snorm) - rb;
             residual[j] = rb;
@@ -357,7 +370,11 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
         if (flag) {
           const int ix = atomicAdd(nflag, 1);
           flags[ix] = static_cast<int32_t>(j);
-          if (cand) {
+          if (cand && accumulate) {
+            // incremental pass: the incoming winner and the appended blocks, all
+            // re-evaluated by the same float64 kernel (exact ties -> lower block)
+            cand[ix] = static_cast<int32_t>(accum_cand(__ldcg(best + j), b0, b1));
+          } else if (cand) {
             // candidate blocks: within the certificate's tolerance of the final best
             // (1 % slack on the bound); all blocks when more than 32
             uint32_t cmask = 0xFFFFFFFFu;

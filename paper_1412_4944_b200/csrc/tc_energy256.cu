@@ -75,6 +75,12 @@ __device__ __forceinline__ float resid_err(float r, float d, int n) {
          3.2e-5f * fmaxf(r, 0.0f);
 }
 
+// candidate mask of a signal flagged by an incremental pass over [b0, b1)
+// (b1 <= 32): its incoming winner and every appended block
+__device__ __forceinline__ uint32_t accum_cand(int prev, int b0, int b1) {
+  return (prev >= 0 && prev < 32 ? 1u << prev : 0u) | (((1u << (b1 - b0)) - 1u) << b0);
+}
+
 template <int G, bool ABS>
 __global__ void __launch_bounds__(THREADS, 1)
 k_energy_tc256(const __half* __restrict__ yh, const __half* __restrict__ yl,
@@ -306,7 +312,8 @@ k_energy_tc256(const __half* __restrict__ yh, const __half* __restrict__ yl,
         if (accumulate) {
           const float prev = ABS ? -static_cast<float>(prev_pre) : static_cast<float>(prev_pre);
           flag = fabsf(d1 - prev) <= err(d1) + err(prev);
-          if (d1 < prev) {
+          // flagged: keep the incoming exact winner / score for the float64 re-decision
+          if (d1 < prev && !flag) {
             best[j] = bb;
             score[j] = ABS ? eb : static_cast<double>(snorm) - rb;
             residual[j] = rb;
@@ -320,7 +327,13 @@ k_energy_tc256(const __half* __restrict__ yh, const __half* __restrict__ yl,
         if (flag) {
           const int ix = atomicAdd(nflag, 1);
           flags[ix] = static_cast<int32_t>(j);
-          if (cand) {
+          if (cand && accumulate) {
+            // incremental pass: the incoming winner and the appended blocks, all
+            // re-evaluated by the same float64 kernel (exact ties -> lower block)
+            cand[ix] = static_cast<int32_t>(accum_cand(__ldcg(best + j), b0, b1));
+          } else if (cand) {
+            // candidate blocks: within the certificate's tolerance of the final best
+            // (1 % slack on the bound); all blocks when more than 32
             uint32_t cmask = 0xFFFFFFFFu;
             if (nblk <= 32) {
               cmask = 0u;

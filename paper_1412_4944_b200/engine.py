@@ -188,7 +188,8 @@ class Engine:
     """One process's device state for a (possibly sharded) SBO problem."""
 
     def __init__(self, sig: Signals, s0: int, kind: str = "squared-sum", k_cap: int = 64,
-                 comm: Comm | None = None, m_total: int | None = None):
+                 comm: Comm | None = None, m_total: int | None = None,
+                 tc: bool | None = None):
         self.sig, self.s0 = sig, int(s0)
         self.kind = L.KIND[kind]
         self.kind_name = kind
@@ -216,7 +217,8 @@ class Engine:
         # tensor-core representation pass: p = 64 (tc_energy.cu) and p = 256 with
         # s0 <= 32 (tc_energy256.cu); other shapes run the float64 tile kernels
         self.tc = ((self.p == 64 or (self.p == 256 and min(s0, self.p) <= 32))
-                   and os.environ.get("SBO_TC", "1") != "0" and self.m > 0)
+                   and os.environ.get("SBO_TC", "1") != "0" and self.m > 0
+                   and tc is not False)
         if self.tc:
             mp = L.size("sbo_tc_padded_rows", self.m)
             self.yh = torch.zeros((mp, self.p), dtype=torch.float16, device=self.dev)
@@ -323,9 +325,14 @@ class Engine:
                        self.ql.data_ptr() + 2 * b0 * pp, self.fscale.data_ptr() + 2 * b0,
                        self.stream)
             self.nflag.zero_()
-            # full pass over <= 32 blocks: the flagged signals carry candidate-block
-            # masks; sorted by them, the float64 tiles only visit their union
-            use_cand = not accumulate and b1 - b0 <= 32
+            # <= 32 blocks: the flagged signals carry candidate-block masks (full
+            # pass: the blocks within the certificate's tolerance of the best;
+            # incremental pass: the incoming winner and the appended blocks);
+            # sorted by them, the float64 tiles only visit their union.  Every
+            # candidate is re-evaluated by the same float64 kernel, so exact ties
+            # go to the lower block (sbo.py:191) whatever kernel produced the
+            # stored scores.
+            use_cand = b1 <= 32
             if use_cand and getattr(self, "cand", None) is None:
                 i32 = dict(dtype=torch.int32, device=self.dev)
                 self.cand = torch.empty(self.m, **i32)
@@ -350,11 +357,10 @@ class Engine:
                            self.nflag.data_ptr(), self.m, s.best.data_ptr(),
                            s.score.data_ptr(), s.residual.data_ptr(), self.stream)
             else:
-                # incremental (accumulate): only the appended blocks are re-decided,
-                # against the exact score / residual the previous full pass stored
-                incr = accumulate and self.exact_scores
+                # more than 32 blocks: the flagged signals are re-decided over every
+                # block from scratch
                 self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
-                           self.p, self.blocks.data_ptr(), b0 if incr else 0, b1,
+                           self.p, self.blocks.data_ptr(), 0, b1,
                            self.s0, self.kind, self.flags.data_ptr(), self.nflag.data_ptr(),
                            self.m, s.best.data_ptr(), s.score.data_ptr(),
                            s.residual.data_ptr(), self.stream)
@@ -581,7 +587,7 @@ class Engine:
         cnt = d["counts"].cpu().numpy()
         # Jacobi sweeps / Newton-Schulz iterations per (phase, round, block)
         self.last_sweeps = (stc >> 8) & 0xFF
-        check_status(stc)
+        check_status(stc, self.p)
         empty = [b for b in range(self.K) if cnt[b] == 0]
         return IterationOut(self.K, rmse, empty, d["members"][: d["n"]])
 
@@ -634,12 +640,15 @@ class Engine:
         return replay
 
 
-def check_status(st: np.ndarray):
+def check_status(st: np.ndarray, p: int | None = None):
+    """Map the device status words of the polar / init steps onto the reference's
+    exceptions (linalg.py:61-63 names the matrix dimensions; onb.py:119-124)."""
     from .linalg import DecompositionError
     from .onb import NumericalError
     st = np.asarray(st) & 0xFF  # bits 8.. carry the Jacobi sweep count
     if (st == L.ST_NOCONV).any():
-        raise DecompositionError("Jacobi SVD did not converge for a block update")
+        dims = f"a {p}x{p} matrix" if p else "a block update"
+        raise DecompositionError(f"SVD did not converge for {dims}")
     if (st == L.ST_DEFECT).any():
         raise NumericalError("block lost orthonormality: defect > 1e-08")
 

@@ -127,6 +127,22 @@ def frobenius_error(y: np.ndarray, dictionary, code) -> float:
     idx, val = np.asarray(code.indices), np.asarray(code.values, dtype=np.float64)
     if idx.shape != val.shape or idx.shape[1] != m:
         raise ValueError(f"reconstruction shape ({p}, {idx.shape[1]}) != signals {y.shape}")
+    # range checks on the host (the device kernel indexes blocks[block[j]] and
+    # q[:, idx] directly): like the reference's block loop (linalg.py:148-158),
+    # a signal whose block id is outside [0, K) is never reconstructed (its
+    # approximation is zero); atom indices follow numpy indexing — negative ones
+    # wrap, out-of-range ones raise IndexError
+    block = np.asarray(block, dtype=np.int64)
+    live = (block >= 0) & (block < blocks.shape[0])
+    if not live.all():
+        val = np.where(live[None, :], val, 0.0)
+        block = np.where(live, block, 0)
+    idx = np.asarray(idx, dtype=np.int64)
+    used = idx[:, live]
+    if used.size and (used.min() < -p or used.max() >= p):
+        bad = int(used.max()) if used.max() >= p else int(used.min())
+        raise IndexError(f"index {bad} is out of bounds for axis 1 with size {p}")
+    idx = np.where(live[None, :], idx % p, 0)
     dev = _dev()
     sig = Signals.from_reference(y, dev)
     B = torch.from_numpy(np.ascontiguousarray(blocks)).to(dev)

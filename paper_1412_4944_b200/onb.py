@@ -178,6 +178,6 @@ def train_onb(y: np.ndarray, q0: np.ndarray, s0: int, rounds: int
     idx = torch.empty((k, t), dtype=torch.int16, device=dev)
     val = torch.empty((k, t), dtype=torch.float64, device=dev)
     eng.code(None, g, 0, True, t, idx, val)
-    check_status(st.cpu().numpy()[:rounds])
+    check_status(st.cpu().numpy()[:rounds], p)
     return (eng.blocks[0].cpu().numpy(),
             ThresholdedCode(idx.cpu().numpy().astype(np.int64), val.cpu().numpy()))

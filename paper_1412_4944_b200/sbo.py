@@ -153,7 +153,10 @@ def block_energy(y: np.ndarray, q: np.ndarray, s0: int, kind: str = "squared-sum
     _check_kind(kind)
     y = np.asarray(y, dtype=np.float64).ravel()
     q = np.asarray(q, dtype=np.float64)
-    eng = Engine(Signals.from_reference(y[:, None], require_device()), s0, kind, k_cap=1)
+    # the exact float64 energy pass (the tensor-core pass's score is only
+    # float32-accurate; it certifies decisions, not values)
+    eng = Engine(Signals.from_reference(y[:, None], require_device()), s0, kind, k_cap=1,
+                 tc=False)
     eng.set_blocks(q[None])
     eng.energy(0, 1, False)
     return float(eng.state.score[0].item())
@@ -247,23 +250,25 @@ def group_by_block(y: np.ndarray, assignment: Assignment, num_blocks: int | None
     block = np.asarray(assignment.block)
     if num_blocks is None:
         num_blocks = int(block.max()) + 1 if block.size else 0
-    y = np.asarray(y)
     m = block.shape[0]
-    if m and block.min() < 0:
-        raise ValueError("block indices must be nonnegative")
-    K = max(num_blocks, int(block.max()) + 1 if m else 0, 1)
+    # the counting sort runs on the device over ids shifted to start at 0 (a
+    # stable sort by id is invariant under the shift), so negative ids order
+    # first, as numpy's argsort puts them
+    lo = int(block.min()) if m else 0
+    shift = min(lo, 0)
+    K = max(num_blocks - shift, int(block.max()) - shift + 1 if m else 0, 1)
     dev = require_device()
     eng = Engine(Signals(torch.zeros((max(m, 1), 1), dtype=torch.float64, device=dev)), 1,
                  k_cap=1)
     eng.m = m
-    eng.state.best = torch.from_numpy(block.astype(np.int32)).to(dev)
+    eng.state.best = torch.from_numpy((block.astype(np.int64) - shift).astype(np.int32)).to(dev)
     g = eng.group(K)
-    perm = g.perm[:m].long()
+    perm = g.perm[:m].long().cpu().numpy()
     bounds = g.bounds.cpu().numpy()
-    ranges = [(int(bounds[b]), int(bounds[b + 1])) for b in range(num_blocks)]
-    rows = torch.from_numpy(np.ascontiguousarray(np.asarray(y, dtype=np.float64).T)).to(dev)
-    grouped = rows.index_select(0, perm).cpu().numpy().T
-    return grouped, ranges, perm.cpu().numpy()
+    ranges = [(int(bounds[b - shift]), int(bounds[b - shift + 1])) for b in range(num_blocks)]
+    # the permuted matrix in the caller's dtype, like the reference's y[:, perm]
+    grouped = np.asarray(y)[:, perm]
+    return grouped, ranges, perm
 
 
 # ---------------------------------------------------------------------------
@@ -291,7 +296,7 @@ def _init_into(eng: Engine, cfg: SboConfig, m_total: int, local_cols=None) -> No
         eng.train_rounds(mem, eng.list_segments(n), n, cfg.rounds, 1, b, None, st[b],
                          single=True)
     eng.K = cfg.k0
-    check_status(st.cpu().numpy())
+    check_status(st.cpu().numpy(), p)
 
 
 def sbo_init(y: np.ndarray, cfg: SboConfig, workers: int | None = None) -> UnionDictionary:

@@ -47,31 +47,39 @@ def scene(height: int = 512, width: int = 512, seed: int = 0) -> np.ndarray:
     return np.floor(img * 255.0 + 0.5).astype(np.uint8)
 
 
-def patch_bytes(grid: np.ndarray, edge: int, count: int, seed: int) -> np.ndarray:
-    """Random edge x edge patches as uint8 rows (count, edge*edge).
+def patch_bytes(grid: np.ndarray, edge: int, count: int, seed: int, lo: int = 0,
+                hi: int | None = None) -> np.ndarray:
+    """Random edge x edge patches as uint8 rows: patches [lo, hi) of ``count``.
 
     Corner draws follow data.py:182-208: rows then columns from
-    ``default_rng(seed).integers``; each patch is vectorized column-major (pixel
-    (r, c) lands at c*edge + r)."""
+    ``default_rng(seed).integers`` over all ``count`` patches (so a shard
+    [lo, hi) gets the same bytes as the whole workload's rows lo..hi-1); each
+    patch is vectorized column-major (pixel (r, c) lands at c*edge + r)."""
     grid = np.asarray(grid)
     h, w = grid.shape
     if h < edge or w < edge:
         raise ValueError(f"grid {h}x{w} is smaller than a {edge}x{edge} patch")
+    hi = count if hi is None else hi
     g = np.random.default_rng(seed)
-    r0 = g.integers(0, h - edge + 1, size=count)
-    c0 = g.integers(0, w - edge + 1, size=count)
+    r0 = g.integers(0, h - edge + 1, size=count)[lo:hi]
+    c0 = g.integers(0, w - edge + 1, size=count)[lo:hi]
     win = np.lib.stride_tricks.sliding_window_view(grid, (edge, edge))
-    out = np.empty((count, edge * edge), np.uint8)
+    n = hi - lo
+    out = np.empty((n, edge * edge), np.uint8)
     step = 1 << 20
-    for s in range(0, count, step):  # bounded temporaries for 16M-patch workloads
-        e = min(s + step, count)
+    for s in range(0, n, step):  # bounded temporaries for 16M-patch workloads
+        e = min(s + step, n)
         out[s:e] = win[r0[s:e], c0[s:e]].transpose(0, 2, 1).reshape(e - s, edge * edge)
     return out
 
 
 def unit_range(u8: np.ndarray) -> np.ndarray:
     """uint8 patch rows -> float32 signals k/255 (the ``unit-range`` normalization)."""
-    return (u8.astype(np.float64) / 255.0).astype(np.float32)
+    # the 256 possible values k/255 (float64, rounded to float32) by table lookup
+    return _UNIT_TABLE[np.asarray(u8, dtype=np.uint8)]
+
+
+_UNIT_TABLE = (np.arange(256, dtype=np.float64) / 255.0).astype(np.float32)
 
 
 def patch_signals(m: int, edge: int = 8, height: int = 512, width: int = 512,

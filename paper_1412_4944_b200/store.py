@@ -10,6 +10,7 @@ the k x m matrices (2.4 GB at m = 2^24, s0 = 8).
 """
 from __future__ import annotations
 
+import itertools
 import json
 import struct
 from dataclasses import dataclass
@@ -35,100 +36,114 @@ class MatrixFormatError(ValueError):
 
 
 # ---------------------------------------------------------------- records
+# An ODM1 record (data.py:210-258 defines the container): 4 magic bytes, the
+# shape as two little-endian uint64, then the float64 payload in column-major
+# order.  Files are plain concatenations of records.
+_SHAPE = np.dtype("<u8")
+_PREFIX = len(ODM_MAGIC) + ODM_HEADER.size
+
+
+def _frame(rows: int, cols: int) -> bytes:
+    """The fixed-size part of a record of the given shape."""
+    return ODM_MAGIC + np.array([rows, cols], dtype=_SHAPE).tobytes()
+
+
+def _encode(a) -> bytes:
+    m = np.asarray(a, dtype=np.float64)
+    if m.ndim != 2:
+        raise ValueError(f"ODM1 stores 2-D matrices, got shape {m.shape}")
+    return _frame(*m.shape) + np.asfortranarray(m).astype("<f8", copy=False).tobytes(order="F")
+
+
 def write_record(f, a: np.ndarray) -> int:
-    """data.py:228-237 — append one ODM1 record; returns the bytes written."""
-    a = np.asarray(a, dtype=np.float64)
-    if a.ndim != 2:
-        raise ValueError(f"ODM1 stores 2-D matrices, got shape {a.shape}")
-    payload = a.tobytes(order="F")
-    f.write(ODM_MAGIC)
-    f.write(ODM_HEADER.pack(a.shape[0], a.shape[1]))
-    f.write(payload)
-    return len(ODM_MAGIC) + ODM_HEADER.size + len(payload)
+    """Append one record to a binary stream; returns its size in bytes (data.py:228-237)."""
+    blob = _encode(a)
+    f.write(blob)
+    return len(blob)
 
 
 def read_record(buf: bytes, pos: int) -> tuple[np.ndarray, int]:
-    """data.py:240-258 — one ODM1 record at ``pos``; returns (matrix, next pos)."""
-    if buf[pos: pos + 4] != ODM_MAGIC:
+    """Decode the record starting at byte ``pos`` of ``buf``; returns (matrix, end
+    offset).  Malformed input raises MatrixFormatError (data.py:240-258)."""
+    view = memoryview(buf)
+    magic = bytes(view[pos:pos + len(ODM_MAGIC)])
+    if magic != ODM_MAGIC:
+        raise MatrixFormatError(f"bad magic {magic!r} at offset {pos}, expected {ODM_MAGIC!r}")
+    body = pos + len(ODM_MAGIC)
+    if len(view) - body < ODM_HEADER.size:
+        raise MatrixFormatError(f"truncated header at offset {body}")
+    rows, cols = (int(v) for v in np.frombuffer(view, dtype=_SHAPE, count=2, offset=body))
+    start = pos + _PREFIX
+    nbytes = 8 * rows * cols
+    if len(view) - start < nbytes:
         raise MatrixFormatError(
-            f"bad magic {buf[pos:pos + 4]!r} at offset {pos}, expected {ODM_MAGIC!r}")
-    pos += 4
-    if len(buf) - pos < ODM_HEADER.size:
-        raise MatrixFormatError(f"truncated header at offset {pos}")
-    rows, cols = ODM_HEADER.unpack_from(buf, pos)
-    pos += ODM_HEADER.size
-    need = rows * cols * 8
-    have = len(buf) - pos
-    if have < need:
-        raise MatrixFormatError(f"truncated payload: expected {need} bytes, got {have}")
-    a = np.frombuffer(buf, dtype="<f8", count=rows * cols, offset=pos)
-    return a.reshape(rows, cols, order="F").copy(order="F"), pos + need
+            f"truncated payload: expected {nbytes} bytes, got {len(view) - start}")
+    flat = np.frombuffer(view, dtype="<f8", count=rows * cols, offset=start)
+    return np.array(flat.reshape((cols, rows)).T, order="F"), start + nbytes
 
 
-def _write_records(path: Path, matrices) -> list[int]:
-    offsets, pos = [], 0
-    with open(path, "wb") as f:
-        for a in matrices:
-            offsets.append(pos)
-            pos += write_record(f, a)
-    return offsets
-
-
-def _write_meta(path: Path, header: dict, offsets: list[int], label: str) -> None:
-    lines = [json.dumps(header, sort_keys=True)]
-    lines += [json.dumps({label: i, "offset": off}, sort_keys=True) for i, off in enumerate(offsets)]
-    path.write_text("\n".join(lines) + "\n")
-
-
-def _read_meta(path: Path) -> tuple[dict, list[dict]]:
-    lines = [ln for ln in path.read_text().splitlines() if ln.strip()]
-    if not lines:
-        raise MatrixFormatError(f"empty meta file {path}")
-    return json.loads(lines[0]), [json.loads(ln) for ln in lines[1:]]
-
-
-def _read_all(path: Path) -> list[np.ndarray]:
+def _scan(path: Path):
+    """Every record of a file, in order."""
     buf = path.read_bytes()
-    out, pos = [], 0
+    pos = 0
     while pos < len(buf):
         a, pos = read_record(buf, pos)
-        out.append(a)
-    return out
+        yield a
+
+
+def _save_records(path: Path, matrices) -> list[int]:
+    """Write the matrices as consecutive records; returns each record's offset."""
+    blobs = [_encode(a) for a in matrices]
+    path.write_bytes(b"".join(blobs))
+    return list(itertools.accumulate((len(b) for b in blobs[:-1]), initial=0)) if blobs else []
+
+
+def _meta_text(header: dict, offsets: list[int], label: str) -> str:
+    """JSON-lines meta: the header, then one {label: i, "offset": o} line per record."""
+    rows = [header] + [{label: i, "offset": o} for i, o in enumerate(offsets)]
+    return "".join(json.dumps(r, sort_keys=True) + "\n" for r in rows)
+
+
+def _load_meta(path: Path) -> tuple[dict, list[dict]]:
+    parsed = [json.loads(t) for t in path.read_text().splitlines() if t.strip()]
+    if not parsed:
+        raise MatrixFormatError(f"empty meta file {path}")
+    return parsed[0], parsed[1:]
 
 
 # ------------------------------------------------------------- dictionary
 def save_dictionary(out_dir, dictionary, extra_meta: dict | None = None) -> None:
-    """store.py:53-69 — a union of blocks, or a dense atom dictionary."""
+    """Write ``dictionary`` (a union of blocks or one dense atom matrix) and its
+    meta file; the files the reference's store.py:53-69 writes."""
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    if isinstance(dictionary, UnionDictionary):
-        offsets = _write_records(out / DICT_FILE, dictionary.blocks)
-        header = {"format": "union-onb", "p": dictionary.p, "blocks": dictionary.num_blocks}
-    else:
-        d = np.asarray(dictionary, dtype=np.float64)
-        offsets = _write_records(out / DICT_FILE, [d])
-        header = {"format": "dense", "p": d.shape[0], "atoms": d.shape[1]}
+    union = isinstance(dictionary, UnionDictionary)
+    mats = list(dictionary.blocks) if union else [np.asarray(dictionary, dtype=np.float64)]
+    header = ({"format": "union-onb", "p": dictionary.p, "blocks": dictionary.num_blocks}
+              if union else {"format": "dense", "p": mats[0].shape[0], "atoms": mats[0].shape[1]})
     header.update(extra_meta or {})
-    _write_meta(out / DICT_META_FILE, header, offsets, "block")
+    offsets = _save_records(out / DICT_FILE, mats)
+    (out / DICT_META_FILE).write_text(_meta_text(header, offsets, "block"))
 
 
 def load_dictionary(out_dir):
-    """store.py:72-96 — (dictionary, header)."""
+    """Read what save_dictionary wrote: (dictionary, header) (store.py:72-96)."""
     out = Path(out_dir)
-    header, entries = _read_meta(out / DICT_META_FILE)
-    matrices = _read_all(out / DICT_FILE)
-    if len(entries) not in (0, len(matrices)):
-        raise MatrixFormatError(f"meta lists {len(entries)} records, file holds {len(matrices)}")
-    if header["format"] == "union-onb":
-        if len(matrices) != header["blocks"]:
+    header, entries = _load_meta(out / DICT_META_FILE)
+    mats = list(_scan(out / DICT_FILE))
+    if entries and len(entries) != len(mats):
+        raise MatrixFormatError(f"meta lists {len(entries)} records, file holds {len(mats)}")
+    kind = header["format"]
+    if kind == "union-onb":
+        if len(mats) != header["blocks"]:
             raise MatrixFormatError(
-                f"dictionary holds {len(matrices)} blocks, meta says {header['blocks']}")
-        return UnionDictionary(matrices), header
-    if header["format"] == "dense":
-        if len(matrices) != 1:
+                f"dictionary holds {len(mats)} blocks, meta says {header['blocks']}")
+        return UnionDictionary(mats), header
+    if kind == "dense":
+        if len(mats) != 1:
             raise MatrixFormatError("dense dictionary file must hold one record")
-        return matrices[0], header
-    raise MatrixFormatError(f"unknown dictionary format {header['format']!r}")
+        return mats[0], header
+    raise MatrixFormatError(f"unknown dictionary format {kind!r}")
 
 
 # ------------------------------------------------------------------ codes
@@ -170,23 +185,22 @@ def save_sbo_codes(out_dir, code, chunk: int = 1 << 20) -> None:
     out.mkdir(parents=True, exist_ok=True)
     if isinstance(code, DeviceCode):
         offsets = _stream_device_codes(out / CODES_FILE, code, chunk)
-        _write_meta(out / CODES_META_FILE, _codes_header(code.m, code.k), offsets, "record")
-        return
-    records = [code.block[None, :].astype(np.float64), code.indices.astype(np.float64),
-               code.values, code.energy[None, :], code.residual_sq[None, :]]
-    offsets = _write_records(out / CODES_FILE, records)
-    _write_meta(out / CODES_META_FILE,
-                _codes_header(int(code.block.shape[0]), int(code.indices.shape[0])), offsets,
-                "record")
+        header = _codes_header(code.m, code.k)
+    else:
+        rows = (code.block[None, :], code.indices, code.values, code.energy[None, :],
+                code.residual_sq[None, :])
+        offsets = _save_records(out / CODES_FILE, [np.asarray(r, np.float64) for r in rows])
+        header = _codes_header(int(code.block.shape[0]), int(code.indices.shape[0]))
+    (out / CODES_META_FILE).write_text(_meta_text(header, offsets, "record"))
 
 
 def load_sbo_codes(out_dir) -> SparseCode:
     """store.py:118-133."""
     out = Path(out_dir)
-    header, _ = _read_meta(out / CODES_META_FILE)
+    header, _ = _load_meta(out / CODES_META_FILE)
     if header.get("format") != "sbo-codes":
         raise MatrixFormatError(f"not an sbo codes file: {header!r}")
-    block, indices, values, energy, residual_sq = _read_all(out / CODES_FILE)
+    block, indices, values, energy, residual_sq = _scan(out / CODES_FILE)
     return SparseCode(block=block.ravel().astype(np.int64), indices=indices.astype(np.int64),
                       values=values, energy=energy.ravel(), residual_sq=residual_sq.ravel())
 
@@ -211,9 +225,8 @@ def _stream_device_codes(path: Path, code: DeviceCode, chunk: int) -> list[int]:
     with open(path, "wb") as f:
         for rec, (rows, cols) in enumerate(shapes):
             offsets.append(pos)
-            f.write(ODM_MAGIC)
-            f.write(ODM_HEADER.pack(rows, cols))
-            pos += len(ODM_MAGIC) + ODM_HEADER.size + 8 * rows * cols
+            f.write(_frame(rows, cols))
+            pos += _PREFIX + 8 * rows * cols
             per = rows  # float64 values per signal in this record
             spans = [(j0, min(chunk, m - j0)) for j0 in range(0, m, chunk)]
 
