@@ -175,6 +175,11 @@ def kernel_families(timer, p, k):
     fam = {"sbo_round_segments": ("k_round64", 2 * p * p + 2 * p * k, 4 * p * p,
                                   "fp64 tensor cores (DMMA)"),
            "sbo_tc_energy": ("k_energy_tc", 2 * p * p, 6 * p * p, "tcgen05 split-fp16"),
+           "sbo_round_code_segments": ("k_round64<code>", 2 * p * p, 2 * p * p,
+                                       "fp64 tensor cores (DMMA)"),
+           # 1280 digit-product columns x 128 rows x 2 int8 ops per signal (outer_i8.cu)
+           "sbo_outer_i8_segments": ("k_outer_i8", 2 * p * k, 2 * 128 * 1280,
+                                     "tcgen05 kind::i8 (exact integer digits)"),
            "sbo_code_segments": ("k_code_f64", 2 * p * p, 2 * p * p, "fp64 CUDA cores"),
            "sbo_residual_segments": ("k_round64<resid>", 2 * p * p, 2 * p * p,
                                      "fp64 tensor cores (DMMA)"),
@@ -329,7 +334,9 @@ def run_reference(a):
 KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1, "sbo_cand_sort": 3,
                     "sbo_outer_segments": 1, "sbo_reduce_segments": 1, "sbo_polar": 2,
                     "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_sum": 2,
-                    "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2}
+                    "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2,
+                    "sbo_round_code_segments": 1, "sbo_outer_i8_segments": 1, "sbo_i8_scan": 1,
+                    "sbo_y_digits": 1}
 
 
 def max_over_ranks(x: float, dist, dev) -> float:
@@ -601,7 +608,7 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
             g, r, c = dev_in[j]
             D.extract_rows(g, D.GRID_U8, a.p_edge, r, c, "unit-range", out=ybuf[j],
                            stream=eng.stream)
-        eng.refresh_signals()  # device-side operand split of the uploaded signals
+        eng.refresh_signals(rescan=False)  # device-side operand split (same digit format)
         return eng.iterate_device(w, a.rounds, dev_draws[j])
 
     # one GPU: each set's step (restore + operand split + iteration) as a CUDA graph

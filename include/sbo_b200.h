@@ -184,6 +184,47 @@ int sbo_round_segments(const void* y, int dtype, int p, const int32_t* order,
                        const int32_t* nseg, int64_t max_seg, const double* blocks,
                        int block_override, int s0, double* partial, void* stream);
 
+/* Coding half of a 1ONB round for p <= 64 (onb.py:170 select_top(Q^T Y)): the
+ * fused round's float64 projection and exact selection, writing the kept pairs
+ * of every signal at column t of the segment order (idx/val rows of stride ld,
+ * the layout of sbo_code_segments with out_by_signal = 0) for
+ * sbo_outer_i8_segments. */
+int sbo_round_code_segments(const void* y, int dtype, int p, const int32_t* order,
+                            const int32_t* seg_block, const int64_t* seg_lo,
+                            const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                            const double* blocks, int block_override, int s0, int64_t ld,
+                            int16_t* idx, double* val, void* stream);
+
+/* Sparse outer products P = Y X^T per block on the tcgen05 tensor cores
+ * (onb.py:127-134; north_star "grouped GEMM Y_j X_j^T"), p = 64, float32
+ * signals: y (as the digit rows of sbo_y_digits) and the code values cut into
+ * 7-bit integer digits (y = Y_int 2^-sy exactly, 5 digits; x rounded to the
+ * 2^-sx grid, 8 digits), digit products accumulated exactly in int32 TMEM and
+ * int64 global accumulators (levels of weight >= 2^-49 relative kept), so P
+ * is independent of the signal order and the segmentation.  P receives
+ * nblocks x p x p float64 (P[b][k][i] = sum y[k] x[i] over the signals of the
+ * segments with seg_block = b; seg_block NULL = every segment in block 0) —
+ * the result sbo_reduce_segments would give.  Codes are read at column t of
+ * the segment order (sbo_round_code_segments).  sy / sx come from sbo_i8_scan:
+ * every |y| < 2^(35 - sy) on the 2^-sy grid, every |x| < 2^(54 - sx).
+ * Workspace: sbo_outer_i8_workspace_bytes(nblocks). */
+size_t sbo_outer_i8_workspace_bytes(int nblocks);
+int sbo_outer_i8_segments(const void* ydig, int p, const int32_t* order,
+                          const int32_t* seg_block, const int64_t* seg_lo,
+                          const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                          int nblocks, int s0, int64_t ld, const int16_t* idx,
+                          const double* val, int sy, int sx, double* P, void* workspace,
+                          size_t ws_bytes, void* stream);
+
+/* Signal-major digit rows of float32 signals for sbo_outer_i8_segments: row s
+ * (320 bytes) = the 5 digit planes Y_a (64 dims each) of y_s = Y_int 2^-sy. */
+int sbo_y_digits(const void* y, int dtype, int64_t m, int p, int sy, void* ydig, void* stream);
+
+/* Digit-format scan of float32 signals (m rows of p): out[0] = smallest E with
+ * every |y| < 2^E, out[1] = smallest exponent of a set mantissa bit among the
+ * nonzero values, out[2..3] = largest ||y||^2 as float64 bits. */
+int sbo_i8_scan(const void* y, int dtype, int64_t m, int p, int32_t* out, void* stream);
+
 /* Squared residuals of represent (sbo.py:213-218) for p <= 64, any s0:
  * every signal of a segment is coded in its segment's block in float64 (exact
  * selection, as sbo_code_segments) and rest_sq[order[t]] receives the energy of

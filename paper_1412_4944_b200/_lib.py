@@ -42,6 +42,12 @@ _SIGS = {
     "sbo_reduce_segments": (I, [P, P, P, I64, I, I, P, P]),
     "sbo_round_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, P, P]),
     "sbo_residual_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, P, P, P]),
+    "sbo_round_code_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, I64, P, P, P]),
+    "sbo_outer_i8_segments": (I, [P, I, P, P, P, P, P, I64, I, I, I64, P, P, I, I, P, P, SZ,
+                                  P]),
+    "sbo_outer_i8_workspace_bytes": (SZ, [I]),
+    "sbo_i8_scan": (I, [P, I, I64, I, P, P]),
+    "sbo_y_digits": (I, [P, I, I64, I, I, P, P]),
     "sbo_gram_workspace_bytes": (SZ, [I64, I, I]),
     "sbo_gram": (I, [P, I, I, P, I64, I, P, P, SZ, P]),
     "sbo_select_top": (I, [P, I64, I, I, I64, P, P, P]),

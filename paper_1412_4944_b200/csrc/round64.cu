@@ -89,7 +89,26 @@ __device__ __forceinline__ int atom_of(int u, int t4) { return 8 * (u >> 1) + 2 
 // MODE_ROUND: coding + P partials; MODE_RESID: coding + squared residuals and
 // scores; MODE_GRAM: P partials with X = Y (the Gram matrix of a member list,
 // onb.py:79-95 via thin_svd(ysub) — no block, no coding)
-constexpr int MODE_ROUND = 0, MODE_RESID = 1, MODE_GRAM = 2;
+// MODE_CODE: coding only, the kept (index, value) pairs written at the signal's
+// segment position (the layout sbo_code_segments writes with out_by_signal = 0),
+// for the tensor-core outer product (outer_i8.cu)
+constexpr int MODE_ROUND = 0, MODE_RESID = 1, MODE_GRAM = 2, MODE_CODE = 3;
+
+// ascending position of atom a = atom_of(u, t4) among the quad's kept atoms
+// (masks[t'] = kept bits of quad lane t', bit u' <-> atom_of(u', t'))
+__device__ __forceinline__ int kept_rank(const uint32_t (&masks)[4], int u, int t4) {
+  const int n = u >> 1, h = u & 1;
+  const uint32_t lower = (1u << (2 * n)) - 1u;  // atoms of column groups < n
+  int r = 0;
+#pragma unroll
+  for (int t2 = 0; t2 < 4; ++t2) {
+    uint32_t below = lower;
+    if (2 * t2 < 2 * t4 + h) below |= 1u << (2 * n);
+    if (2 * t2 + 1 < 2 * t4 + h) below |= 1u << (2 * n + 1);
+    r += __popc(masks[t2] & below);
+  }
+  return r;
+}
 
 template <typename TY, int MODE>
 __global__ void __launch_bounds__(kThreads, 2) k_round64(
@@ -97,9 +116,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
     const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
     const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg,
     const double* __restrict__ blocks, int block_override, int k, double* partial,
-    double* rest_sq, int kind, double* score) {
+    double* rest_sq, int kind, double* score, int64_t ld, int16_t* cidx, double* cval) {
   constexpr int NB = Stage<TY>::NB, YLD = Stage<TY>::YLD;
   constexpr bool kResid = MODE == MODE_RESID;
+  constexpr bool kCode = MODE == MODE_CODE;
+  constexpr bool kOuter = MODE == MODE_ROUND || MODE == MODE_GRAM;
   if (static_cast<int>(blockIdx.x) >= *nseg) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const Layout<TY> L;
@@ -333,7 +354,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       }
       __syncwarp();
     }
-    if constexpr (kResid) {
+    if constexpr (kCode) {
+      // the kept pairs in ascending atom order at column t of the segment order
+      uint32_t masks[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) masks[x] = __shfl_sync(0xffffffffu, mask, (lane & ~3) | x);
+      if (act) {
+        const int64_t col = t0 + s;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if ((mask >> u) & 1u) {
+            const int at = kept_rank(masks, u, t4);
+            cidx[at * ld + col] = static_cast<int16_t>(atom_of(u, t4));
+            cval[at * ld + col] = c[u >> 1][u & 1];
+          }
+        }
+      }
+    } else if constexpr (kResid) {
       // every lane takes part in the quad sum (full-mask shuffles), the
       // fallback's exact value wins where it was computed
       double d = 0.0, e = 0.0;
@@ -353,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
         rest_sq[rows[s]] = rest;
         if (score) score[rows[s]] = e;
       }
-    } else {
+    } else if constexpr (MODE == MODE_ROUND) {
       // X = the kept coefficients, zeros elsewhere (fragment layout -> rows of X)
       double* xr = X + s * LD + 2 * t4;
 #pragma unroll
@@ -363,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
                          ((mask >> (2 * n + 1)) & 1u) ? c[n][1] : 0.0);
     }
     }  // MODE != MODE_GRAM
-    if constexpr (!kResid) {
+    if constexpr (kOuter) {
       __syncthreads();
       // P[kk][i] += sum_s Y[s][kk] X[s][i] on DMMA, signals in order (inactive
       // rows are zero in both Y and X)
@@ -377,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_round64(
       }
     }
   }
-  if constexpr (!kResid) {
+  if constexpr (kOuter) {
     double* out = partial + static_cast<int64_t>(seg) * p * p;
     const int row = 8 * warp + g;
 #pragma unroll
@@ -394,15 +431,17 @@ template <typename TY, int MODE>
 int launch(const void* yv, int p, const int32_t* order, const int32_t* seg_block,
            const int64_t* seg_lo, const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
            const double* blocks, int block_override, int k, double* partial, double* rest_sq,
-           int kind, double* score, cudaStream_t st) {
+           int kind, double* score, cudaStream_t st, int64_t ld = 0, int16_t* cidx = nullptr,
+           double* cval = nullptr) {
   const Layout<TY> L;
   cudaFuncSetAttribute(k_round64<TY, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
   k_round64<TY, MODE><<<static_cast<unsigned>(max_seg), kThreads, L.bytes, st>>>(
       static_cast<const TY*>(yv), p, order, seg_block, seg_lo, seg_hi, nseg, blocks,
-      block_override, k, partial, rest_sq, kind, score);
+      block_override, k, partial, rest_sq, kind, score, ld, cidx, cval);
   return check_launch(MODE == MODE_RESID ? "k_round64<resid>"
-                                         : (MODE == MODE_GRAM ? "k_round64<gram>" : "k_round64"));
+                      : MODE == MODE_GRAM ? "k_round64<gram>"
+                      : MODE == MODE_CODE ? "k_round64<code>" : "k_round64");
 }
 
 int check(int dtype, int p, int s0) {
@@ -469,4 +508,25 @@ int sbo_gram_partials64(const void* y, int dtype, int p, const int32_t* members,
                                                    nseg, max_seg, nullptr, 0, 1, partial,
                                                    nullptr, SBO_KIND_SQUARED_SUM, nullptr,
                                                    as_stream(stream));
+}
+
+extern "C" int sbo_round_code_segments(const void* y, int dtype, int p, const int32_t* order,
+                                       const int32_t* seg_block, const int64_t* seg_lo,
+                                       const int64_t* seg_hi, const int32_t* nseg,
+                                       int64_t max_seg, const double* blocks, int block_override,
+                                       int s0, int64_t ld, int16_t* idx, double* val,
+                                       void* stream) {
+  if (int rc = r64::check(dtype, p, s0)) return rc;
+  if (!idx || !val) return fail(SBO_EINVAL, "idx and val are required");
+  if (max_seg <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  return dtype == SBO_F32
+             ? r64::launch<float, r64::MODE_CODE>(y, p, order, seg_block, seg_lo, seg_hi, nseg,
+                                                  max_seg, blocks, block_override, k, nullptr,
+                                                  nullptr, SBO_KIND_SQUARED_SUM, nullptr,
+                                                  as_stream(stream), ld, idx, val)
+             : r64::launch<double, r64::MODE_CODE>(y, p, order, seg_block, seg_lo, seg_hi, nseg,
+                                                   max_seg, blocks, block_override, k, nullptr,
+                                                   nullptr, SBO_KIND_SQUARED_SUM, nullptr,
+                                                   as_stream(stream), ld, idx, val);
 }

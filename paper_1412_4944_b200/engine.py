@@ -216,6 +216,7 @@ class Engine:
         # tensor-core representation (p = 64): split-fp16 operands, built once
         # tensor-core representation pass: p = 64 (tc_energy.cu) and p = 256 with
         # s0 <= 32 (tc_energy256.cu); other shapes run the float64 tile kernels
+        self.i8 = None  # (sy, sx) digit scales of the tensor-core outer product
         self.tc = ((self.p == 64 or (self.p == 256 and min(s0, self.p) <= 32))
                    and os.environ.get("SBO_TC", "1") != "0" and self.m > 0
                    and tc is not False)
@@ -227,14 +228,46 @@ class Engine:
             self.flags = torch.empty(self.m, dtype=torch.int32, device=self.dev)
             self.nflag = torch.zeros(1, dtype=torch.int32, device=self.dev)
             self._alloc_tc_blocks(self.k_cap)
-            self.refresh_signals()
+        self.refresh_signals()
 
-    def refresh_signals(self):
-        """Re-derive the tensor-core operands (split fp16) after the signals changed."""
+    def refresh_signals(self, rescan: bool = True):
+        """Re-derive the tensor-core operands (split fp16) after the signals changed;
+        ``rescan`` re-checks the integer-digit format of the training rounds (a
+        host synchronisation: pass False when the new signals are known to share
+        the old ones' format, e.g. inside a captured CUDA graph)."""
         if self.tc:
             self._call("sbo_tc_split_signals", self.sig.y.data_ptr(), self.sig.code, self.m,
                        self.p, self.yh.data_ptr(), self.yl.data_ptr(), self.escale.data_ptr(),
                        self.stream)
+        if rescan:
+            self._scan_digits()
+
+    def _scan_digits(self):
+        """Digit formats of the tensor-core outer product (outer_i8.cu): p = 64,
+        float32 signals whose values all sit exactly on one fixed-point grid of 35
+        bits (unit-range image patches do); otherwise the rounds run the fused
+        float64 DMMA kernel."""
+        self.i8 = None
+        if (self.p != 64 or self.sig.code != L.F32 or self.m == 0
+                or os.environ.get("SBO_I8", "0") != "1"):
+            return
+        out = torch.empty(4, dtype=torch.int32, device=self.dev)
+        self._call("sbo_i8_scan", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
+                   out.data_ptr(), self.stream)
+        emax, lsb = (int(v) for v in out[:2].cpu())
+        norm2 = float(out[2:].view(torch.float64).item())
+        if emax < -900:  # every signal is zero
+            return
+        sy = 35 - emax
+        if lsb + sy < 0 or sy > 126 + 35:
+            return  # some value is finer than the 35-bit grid: not exact
+        xmax = math.sqrt(norm2) * (1.0 + 1e-6)  # |x| <= ||y|| (orthonormal blocks)
+        ex = math.floor(math.log2(xmax)) + 1 if xmax > 0 else 0
+        self.i8 = (sy, 54 - ex)
+        # signal-major digit rows (5 planes x 64 dims per signal), built once
+        self.ydig = torch.empty((self.m, 5 * 64), dtype=torch.int8, device=self.dev)
+        self._call("sbo_y_digits", self.sig.y.data_ptr(), self.sig.code, self.m, self.p, sy,
+                   self.ydig.data_ptr(), self.stream)
 
     def _alloc_tc_blocks(self, cap: int):
         self.qh = torch.zeros((cap, self.p, self.p), dtype=torch.float16, device=self.dev)
@@ -424,7 +457,10 @@ class Engine:
 
         single=True: one block (first_block) over a member list of n entries."""
         p = self.p
-        partial = self.scratch.get("partial", 8 * g.max_seg * p * p)
+        partial = (self.scratch.get("partial", 8 * g.max_seg * p * p) if self.i8 is None
+                   else None)
+        i8_ws = (self.scratch.get("i8", L.size("sbo_outer_i8_workspace_bytes", nblocks))
+                 if self.i8 is not None else None)
         P = self.scratch.get("P", 8 * nblocks * p * p)
         ld = max(n, 1)
         idx = self.scratch.get("tr_idx", 2 * self.k * ld).view(torch.int16)
@@ -434,7 +470,21 @@ class Engine:
         fused = p <= 64 and os.environ.get("SBO_FUSED_ROUND", "1") != "0"
         override = first_block if single else -1
         for r in range(rounds):
-            if fused:  # coding + P partials in one pass per segment
+            if self.i8 is not None:
+                # coding (float64 DMMA projection, exact selection) writes the kept
+                # pairs; P = Y X^T on tcgen05 from exact integer digits
+                self._call("sbo_round_code_segments", self.sig.y.data_ptr(), self.sig.code, p,
+                           _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
+                           g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
+                           self.blocks.data_ptr(), override, self.s0, ld, idx.data_ptr(),
+                           val.data_ptr(), self.stream, units=n)
+                self._call("sbo_outer_i8_segments", self.ydig.data_ptr(), p, _ptr(order),
+                           None if single else g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
+                           g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, nblocks,
+                           self.s0, ld, idx.data_ptr(), val.data_ptr(), self.i8[0],
+                           self.i8[1], Pt.data_ptr(), i8_ws.data_ptr(), i8_ws.numel(),
+                           self.stream, units=n)
+            elif fused:  # coding + P partials in one pass per segment
                 self._call("sbo_round_segments", self.sig.y.data_ptr(), self.sig.code, p,
                            _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
                            g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
@@ -446,9 +496,10 @@ class Engine:
                            _ptr(order), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
                            g.nseg.data_ptr(), g.max_seg, self.s0, ld, idx.data_ptr(),
                            val.data_ptr(), partial.data_ptr(), self.stream)
-            self._call("sbo_reduce_segments", partial.data_ptr(),
-                       None if single else g.seg_block.data_ptr(), g.nseg.data_ptr(),
-                       g.max_seg, nblocks, p, Pt.data_ptr(), self.stream)
+            if self.i8 is None:
+                self._call("sbo_reduce_segments", partial.data_ptr(),
+                           None if single else g.seg_block.data_ptr(), g.nseg.data_ptr(),
+                           g.max_seg, nblocks, p, Pt.data_ptr(), self.stream)
             self.comm.allreduce(Pt)
             self._call("sbo_polar", Pt.data_ptr(), nblocks, p, _ptr(counts),
                        self.block_ptr(first_block), self.v_ptr(first_block), None,
