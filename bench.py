@@ -336,7 +336,7 @@ KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1
                     "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_sum": 2,
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2,
                     "sbo_round_code_segments": 1, "sbo_outer_i8_segments": 1, "sbo_i8_scan": 1,
-                    "sbo_y_digits": 1}
+                    "sbo_y_digits": 1, "sbo_y_tiles": 1}
 
 
 def max_over_ranks(x: float, dist, dev) -> float:

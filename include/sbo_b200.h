@@ -197,7 +197,8 @@ int sbo_round_code_segments(const void* y, int dtype, int p, const int32_t* orde
 
 /* Sparse outer products P = Y X^T per block on the tcgen05 tensor cores
  * (onb.py:127-134; north_star "grouped GEMM Y_j X_j^T"), p = 64, float32
- * signals: y (as the digit rows of sbo_y_digits) and the code values cut into
+ * signals: y (as the transposed digit tiles of sbo_y_tiles, built once per
+ * grouping) and the code values cut into
  * 7-bit integer digits (y = Y_int 2^-sy exactly, 5 digits; x rounded to the
  * 2^-sx grid, 8 digits), digit products accumulated exactly in int32 TMEM and
  * int64 global accumulators (levels of weight >= 2^-49 relative kept), so P
@@ -209,12 +210,21 @@ int sbo_round_code_segments(const void* y, int dtype, int p, const int32_t* orde
  * every |y| < 2^(35 - sy) on the 2^-sy grid, every |x| < 2^(54 - sx).
  * Workspace: sbo_outer_i8_workspace_bytes(nblocks). */
 size_t sbo_outer_i8_workspace_bytes(int nblocks);
-int sbo_outer_i8_segments(const void* ydig, int p, const int32_t* order,
-                          const int32_t* seg_block, const int64_t* seg_lo,
+int sbo_outer_i8_segments(const void* ytiles, int p, const int32_t* seg_block,
+                          const int64_t* seg_lo,
                           const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
                           int nblocks, int s0, int64_t ld, const int16_t* idx,
                           const double* val, int sy, int sx, double* P, void* workspace,
                           size_t ws_bytes, void* stream);
+
+/* Transposed digit tiles of a segment table for sbo_outer_i8_segments: per
+ * (segment, 128-position chunk) in segment order, the 5 digit planes of the
+ * signals order[t] as [64 dims][128 signals] int8 (40 KB, the kernel's shared
+ * memory image).  tiles: sbo_y_tiles_bytes(n, max_seg) bytes (n = positions). */
+size_t sbo_y_tiles_bytes(int64_t n, int64_t max_seg);
+int sbo_y_tiles(const void* ydig, const int32_t* order, const int64_t* seg_lo,
+                const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg, void* tiles,
+                void* stream);
 
 /* Signal-major digit rows of float32 signals for sbo_outer_i8_segments: row s
  * (320 bytes) = the 5 digit planes Y_a (64 dims each) of y_s = Y_int 2^-sy. */

@@ -49,18 +49,37 @@ constexpr int EPI_DIMS = 8;             // dims per TMEM read batch of the epilo
 constexpr int64_t RUN_MAX = 1 << 15;    // signals per TMEM accumulation (int32 bound:
                                         // <= 4 digit pairs x 127 x 64 per signal and region)
 
+constexpr uint32_t YTILE = YD * PLANE;  // one transposed Y digit tile: 40 KB
+
 struct Smem {
   int8_t x[2][XD * PLANE];
-  int8_t y[2][YD * PLANE];
-  int64_t rows[2][TS];  // the tile's signal rows (order[t])
-  uint64_t full[2], empty[2], run_done;
+  int8_t y[2][YTILE];
+  uint64_t full[2], fully[2], empty[2], run_done;
   uint32_t tmem;
+  int base;
 };
 
 // the CTA's contiguous range of segments
 __device__ __forceinline__ void seg_range(int nseg, int& s0, int& s1) {
   s0 = static_cast<int>(static_cast<int64_t>(nseg) * blockIdx.x / gridDim.x);
   s1 = static_cast<int>(static_cast<int64_t>(nseg) * (blockIdx.x + 1) / gridDim.x);
+}
+
+// tile slot of segment s0's first tile: tiles of the segments before it (each
+// segment's tiles start at a fresh 128-signal slot); every thread of the CTA
+// calls it, the result is valid in all of them
+__device__ int tile_base(const int64_t* seg_lo, const int64_t* seg_hi, int s0, int* slot) {
+  if (threadIdx.x == 0) *slot = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int s = threadIdx.x; s < s0; s += blockDim.x)
+    mine += static_cast<int>(ceil_div(seg_hi[s] - seg_lo[s], TS));
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(slot, mine);
+  __syncthreads();
+  const int b = *slot;
+  __syncthreads();
+  return b;
 }
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 
@@ -108,8 +127,8 @@ struct Ring {
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
-k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
-           const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
+k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_block,
+           const int64_t* __restrict__ seg_lo,
            const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg_p, int k,
            int64_t ld, const int16_t* __restrict__ idx, const double* __restrict__ val,
            double xscale, unsigned long long* __restrict__ acc64) {
@@ -120,6 +139,7 @@ k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
   if (tid == 0) {
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&S->full[s], 1);
+      sm100::mbar_init(&S->fully[s], 1);
       sm100::mbar_init(&S->empty[s], 1);
     }
     sm100::mbar_init(&S->run_done, 1);
@@ -130,35 +150,25 @@ k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = S->tmem;
+  int sa, sb;
+  seg_range(nseg, sa, sb);
+  const int slot0 = tile_base(seg_lo, seg_hi, sa, &S->base);
 
   if (warp >= 4) {  // ------------------------------------------------ producers
-    // Every global load of a tile is issued before the wait for its stage, so
-    // the loads' latency overlaps the previous tile's MMAs: the tile's row
-    // indices (one round trip, via shared memory), then all of this thread's
-    // digit words and its first code pairs in flight at once.
-    //   Y: item = (signal quad q, dim word w): 5 planes x 4 signals words of the
-    //      signal-major digit rows (sbo_y_digits), each 4 x 4 byte block
-    //      transposed with PRMT into 4 plane rows (dims) x 4 signals.
+    //   Y: the tile's transposed digit planes (sbo_y_tiles, once per grouping)
+    //      arrive by one bulk copy on fully[stage];
     //   X: zero planes, then each kept pair's 8 balanced digits; thread (sl, r0)
-    //      takes code rows r0, r0 + 3, ... of signal sl.
+    //      takes code rows r0, r0 + 3, ... of signal sl.  The first code rows of
+    //      the next tile are loaded before the wait for its stage.
     const int pt = tid - 128;
-    // Y item = (signal quad q, plane a, dim group g of 16): 4 x 16-B loads (one
-    // per signal; 20 consecutive items cover a signal's 320-B digit row), four
-    // 4 x 4 byte transposes, 16 word stores
-    constexpr int NIT = (TS / 4) * YD * 4;                   // 640 per tile
-    constexpr int YI = (NIT + NPROD - 1) / NPROD;            // per thread (2)
     constexpr int XPRE = 3;                                  // code rows preloaded
     const int sl_x = pt & (TS - 1), r0_x = pt >> 7;          // 384 = 3 x 128
     Ring r;
-    int sa, sb;
-    seg_range(nseg, sa, sb);
+    int slot = slot0;
     for (int seg = sa; seg < sb; ++seg) {
       const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
-      for (int64_t t0 = lo; t0 < hi; t0 += TS) {
+      for (int64_t t0 = lo; t0 < hi; t0 += TS, ++slot) {
         const int n = static_cast<int>(min64(TS, hi - t0));
-        int64_t* srow = S->rows[r.i];
-        if (pt < TS) srow[pt] = pt < n ? (order ? static_cast<int64_t>(__ldg(order + t0 + pt))
-                                                : t0 + pt) : -1;
         int pj[XPRE];
         double pv[XPRE];
 #pragma unroll
@@ -172,47 +182,16 @@ k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
             pv[c] = __ldg(val + col);
           }
         }
-        asm volatile("bar.sync 2, %0;" ::"r"(NPROD));  // srow visible
-        uint4 wv[YI][4];
-#pragma unroll
-        for (int v = 0; v < YI; ++v) {
-          const int it = pt + v * NPROD;
-          const int q = it / 20, ag = it - q * 20;  // ag = 4 a + g
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int sl = 4 * q + u;
-            wv[v][u] = make_uint4(0u, 0u, 0u, 0u);
-            if (it < NIT && sl < n)
-              wv[v][u] = __ldg(reinterpret_cast<const uint4*>(ydig + srow[sl] * (YD * P)) + ag);
-          }
-        }
         sm100::mbar_wait(&S->empty[r.i], r.ph ^ 1u);
+        if (pt == 0) {
+          sm100::mbar_expect_tx(&S->fully[r.i], YTILE);
+          sm100::bulk_g2s(S->y[r.i], ytiles + static_cast<int64_t>(slot) * YTILE, YTILE,
+                          &S->fully[r.i]);
+        }
         int8_t* xs = S->x[r.i];
-        int8_t* ys = S->y[r.i];
         {
           uint4* z = reinterpret_cast<uint4*>(xs);
           for (int e = pt; e < XD * PLANE / 16; e += NPROD) z[e] = make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int v = 0; v < YI; ++v) {
-          const int it = pt + v * NPROD;
-          if (it >= NIT) break;
-          const int q = it / 20, ag = it - q * 20, a = ag >> 2, g = ag & 3;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {  // dims 16 g + 4 h .. + 3
-            const uint32_t r0 = (&wv[v][0].x)[h], r1 = (&wv[v][1].x)[h];
-            const uint32_t r2 = (&wv[v][2].x)[h], r3 = (&wv[v][3].x)[h];
-            const uint32_t t0_ = __byte_perm(r0, r1, 0x5140);
-            const uint32_t t1_ = __byte_perm(r2, r3, 0x5140);
-            const uint32_t t2_ = __byte_perm(r0, r1, 0x7362);
-            const uint32_t t3_ = __byte_perm(r2, r3, 0x7362);
-            const uint32_t c[4] = {__byte_perm(t0_, t1_, 0x5410), __byte_perm(t0_, t1_, 0x7632),
-                                   __byte_perm(t2_, t3_, 0x5410), __byte_perm(t2_, t3_, 0x7632)};
-            const int row0 = 16 * g + 4 * h;
-#pragma unroll
-            for (int d = 0; d < 4; ++d)
-              *reinterpret_cast<uint32_t*>(ys + a * PLANE + plane_off(row0 + d, 4 * q)) = c[d];
-          }
         }
         asm volatile("bar.sync 2, %0;" ::"r"(NPROD));  // X planes zeroed
         auto put = [&](int j, double x, int sl) {
@@ -247,8 +226,6 @@ k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
     Ring r;
     uint32_t run_ph = 0;
     const int e = tid;  // TMEM lane of this epilogue thread
-    int sa, sb;
-    seg_range(nseg, sa, sb);
     int seg = sa;
     while (seg < sb) {
       const int blk = seg_block ? seg_block[seg] : 0;
@@ -269,6 +246,7 @@ k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
           for (int sg = seg; sg < send; ++sg) {
             for (int64_t t0 = seg_lo[sg]; t0 < seg_hi[sg]; t0 += TS) {
               sm100::mbar_wait(&S->full[r.i], r.ph);
+              sm100::mbar_wait(&S->fully[r.i], r.ph);
               sm100::tc_fence_after();
               const uint32_t xb = sm100::smem_u32(S->x[r.i]);
               const uint32_t yb = sm100::smem_u32(S->y[r.i]);
@@ -349,6 +327,66 @@ k_outer_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
   }
   __syncthreads();
   if (warp == 1) sm100::tmem_dealloc(tmem, 512);
+}
+
+// Transposed Y digit tiles, once per grouping (the order does not change across
+// a grouping's training rounds): tile slot = (segment, 128-position chunk) in
+// segment order, 5 planes x [64 dims][128 signals] int8, SW128-swizzled: the
+// exact shared-memory image k_outer_i8 bulk-copies.  Item = (signal quad q, dim
+// word w): 5 planes x 4 signals words of the signal-major digit rows, each 4 x 4
+// byte block transposed with PRMT.
+constexpr int YT_THREADS = 256;
+
+__global__ void __launch_bounds__(YT_THREADS)
+k_y_tiles(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
+          const int64_t* __restrict__ seg_lo, const int64_t* __restrict__ seg_hi,
+          const int32_t* __restrict__ nseg_p, int8_t* __restrict__ tiles) {
+  __shared__ __align__(16) int8_t st[YTILE];
+  __shared__ int64_t srow[TS];
+  __shared__ int base;
+  const int nseg = *nseg_p;
+  int sa, sb;
+  seg_range(nseg, sa, sb);
+  int slot = tile_base(seg_lo, seg_hi, sa, &base);
+  const int tid = threadIdx.x;
+  for (int seg = sa; seg < sb; ++seg) {
+    const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+    for (int64_t t0 = lo; t0 < hi; t0 += TS, ++slot) {
+      const int n = static_cast<int>(min64(TS, hi - t0));
+      if (tid < TS) srow[tid] = tid < n ? (order ? static_cast<int64_t>(order[t0 + tid]) : t0 + tid)
+                                        : -1;
+      __syncthreads();
+      for (int it = tid; it < (TS / 4) * (P / 4); it += YT_THREADS) {
+        const int w = it & 15, q = it >> 4;
+        uint32_t wv[YD][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int sl = 4 * q + u;
+          const uint32_t* src =
+              reinterpret_cast<const uint32_t*>(ydig + (sl < n ? srow[sl] : 0) * (YD * P)) + w;
+#pragma unroll
+          for (int a = 0; a < YD; ++a) wv[a][u] = sl < n ? __ldg(src + a * (P / 4)) : 0u;
+        }
+#pragma unroll
+        for (int a = 0; a < YD; ++a) {
+          const uint32_t t0_ = __byte_perm(wv[a][0], wv[a][1], 0x5140);
+          const uint32_t t1_ = __byte_perm(wv[a][2], wv[a][3], 0x5140);
+          const uint32_t t2_ = __byte_perm(wv[a][0], wv[a][1], 0x7362);
+          const uint32_t t3_ = __byte_perm(wv[a][2], wv[a][3], 0x7362);
+          const uint32_t c[4] = {__byte_perm(t0_, t1_, 0x5410), __byte_perm(t0_, t1_, 0x7632),
+                                 __byte_perm(t2_, t3_, 0x5410), __byte_perm(t2_, t3_, 0x7632)};
+#pragma unroll
+          for (int d = 0; d < 4; ++d)
+            *reinterpret_cast<uint32_t*>(st + a * PLANE + plane_off(4 * w + d, 4 * q)) = c[d];
+        }
+      }
+      __syncthreads();
+      uint4* dst = reinterpret_cast<uint4*>(tiles + static_cast<int64_t>(slot) * YTILE);
+      const uint4* srcs = reinterpret_cast<const uint4*>(st);
+      for (int e = tid; e < static_cast<int>(YTILE / 16); e += YT_THREADS) dst[e] = srcs[e];
+      __syncthreads();
+    }
+  }
 }
 
 // P[b][i][j] = 2^(77-sy-sx) (HI 128^-3 + LO 128^-7) from the int64 accumulators
@@ -459,12 +497,31 @@ extern "C" int sbo_y_digits(const void* y, int dtype, int64_t m, int p, int sy, 
   return check_launch("k_y_digits");
 }
 
+extern "C" size_t sbo_y_tiles_bytes(int64_t n, int64_t max_seg) {
+  return static_cast<size_t>(ceil_div(n > 0 ? n : 0, oi8::TS) + (max_seg > 0 ? max_seg : 0)) *
+         oi8::YTILE;
+}
+
+extern "C" int sbo_y_tiles(const void* ydig, const int32_t* order, const int64_t* seg_lo,
+                           const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                           void* tiles, void* stream) {
+  if (!ydig || !tiles) return fail(SBO_EINVAL, "bad arguments");
+  if (max_seg <= 0) return SBO_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(min64(max_seg, 4 * sms));
+  oi8::k_y_tiles<<<grid, oi8::YT_THREADS, 0, as_stream(stream)>>>(
+      static_cast<const int8_t*>(ydig), order, seg_lo, seg_hi, nseg, static_cast<int8_t*>(tiles));
+  return check_launch("k_y_tiles");
+}
+
 extern "C" size_t sbo_outer_i8_workspace_bytes(int nblocks) {
   return static_cast<size_t>(nblocks > 0 ? nblocks : 0) * 2 * 64 * 64 * sizeof(long long);
 }
 
-extern "C" int sbo_outer_i8_segments(const void* ydig, int p, const int32_t* order,
-                                     const int32_t* seg_block, const int64_t* seg_lo,
+extern "C" int sbo_outer_i8_segments(const void* ytiles, int p, const int32_t* seg_block,
+                                     const int64_t* seg_lo,
                                      const int64_t* seg_hi, const int32_t* nseg,
                                      int64_t max_seg, int nblocks, int s0, int64_t ld,
                                      const int16_t* idx, const double* val, int sy, int sx,
@@ -491,7 +548,7 @@ extern "C" int sbo_outer_i8_segments(const void* ydig, int p, const int32_t* ord
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = static_cast<unsigned>(min64(max_seg, sms));
     oi8::k_outer_i8<<<grid, oi8::THREADS, oi8::SMEM_BYTES, st>>>(
-        static_cast<const int8_t*>(ydig), order, seg_block, seg_lo, seg_hi, nseg, k, ld, idx,
+        static_cast<const int8_t*>(ytiles), seg_block, seg_lo, seg_hi, nseg, k, ld, idx,
         val, ldexp(1.0, sx), acc);
     if (int rc = check_launch("k_outer_i8")) return rc;
   }

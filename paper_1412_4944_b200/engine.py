@@ -249,7 +249,7 @@ class Engine:
         float64 DMMA kernel."""
         self.i8 = None
         if (self.p != 64 or self.sig.code != L.F32 or self.m == 0
-                or os.environ.get("SBO_I8", "0") != "1"):
+                or os.environ.get("SBO_I8", "1") != "1"):
             return
         out = torch.empty(4, dtype=torch.int32, device=self.dev)
         self._call("sbo_i8_scan", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
@@ -459,8 +459,15 @@ class Engine:
         p = self.p
         partial = (self.scratch.get("partial", 8 * g.max_seg * p * p) if self.i8 is None
                    else None)
-        i8_ws = (self.scratch.get("i8", L.size("sbo_outer_i8_workspace_bytes", nblocks))
-                 if self.i8 is not None else None)
+        i8_ws = ytiles = None
+        if self.i8 is not None:
+            i8_ws = self.scratch.get("i8", L.size("sbo_outer_i8_workspace_bytes", nblocks))
+            # transposed digit tiles of this grouping, shared by its R rounds
+            ytiles = self.scratch.get("ytiles_list" if single else "ytiles",
+                                      L.size("sbo_y_tiles_bytes", n, g.max_seg))
+            self._call("sbo_y_tiles", self.ydig.data_ptr(), _ptr(order), g.seg_lo.data_ptr(),
+                       g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, ytiles.data_ptr(),
+                       self.stream, units=n)
         P = self.scratch.get("P", 8 * nblocks * p * p)
         ld = max(n, 1)
         idx = self.scratch.get("tr_idx", 2 * self.k * ld).view(torch.int16)
@@ -478,7 +485,7 @@ class Engine:
                            g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
                            self.blocks.data_ptr(), override, self.s0, ld, idx.data_ptr(),
                            val.data_ptr(), self.stream, units=n)
-                self._call("sbo_outer_i8_segments", self.ydig.data_ptr(), p, _ptr(order),
+                self._call("sbo_outer_i8_segments", ytiles.data_ptr(), p,
                            None if single else g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
                            g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, nblocks,
                            self.s0, ld, idx.data_ptr(), val.data_ptr(), self.i8[0],
