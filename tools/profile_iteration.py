@@ -17,14 +17,15 @@ from paper_1412_4944_b200.sbo import SboConfig, _block_rng, _init_into  # noqa: 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--m", type=int, default=1 << 20)
+    ap.add_argument("--m", type=int, default=1 << 24)
     ap.add_argument("--K", type=int, default=16)
     ap.add_argument("--iters", type=int, default=1)
     ap.add_argument("--p-edge", type=int, default=8)
     ap.add_argument("--s0", type=int, default=8)
+    ap.add_argument("--scene", type=int, default=4096)
     a = ap.parse_args()
     dev = require_device()
-    rows = signals.unit_range(signals.patch_bytes(signals.scene(2048, 2048, 0), a.p_edge, a.m, 11))
+    rows = signals.unit_range(signals.patch_bytes(signals.scene(a.scene, a.scene, 0), a.p_edge, a.m, 11))
     eng = Engine(Signals.from_rows(rows, dev), a.s0, k_cap=a.K)
     _init_into(eng, SboConfig(s0=a.s0, k0=a.K - 1, p0=4096, rounds=6, k_max=a.K, seed=1), a.m)
     eng.represent_full()
