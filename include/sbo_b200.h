@@ -195,6 +195,28 @@ int sbo_round_code_segments(const void* y, int dtype, int p, const int32_t* orde
                             const double* blocks, int block_override, int s0, int64_t ld,
                             int16_t* idx, double* val, void* stream);
 
+/* The 1ONB round's coding (onb.py:170-171: select_top(Q^T Y)) and represent's
+ * residual pass (sbo.py:207-218) for p = 64, 1 <= s0 <= 32, on the tcgen05
+ * tensor cores: the projection is computed exactly from integer digits
+ * (tcgen05.mma kind::i8; y as the sbo_y_digits rows, y = Y_int 2^-sy; each
+ * block entry rounded to 2^-54 in 8 digits; digit levels of weight >= 2^-49
+ * relative kept), then the exact top-s0 selection (ties -> lower atom).
+ * Replaces the DMMA projection of sbo_round_code_segments /
+ * sbo_residual_segments.  Segments as sbo_round_code_segments; blocks holds
+ * nblocks blocks (block_override >= 0: every segment uses that block).
+ * mode 0 (code): the kept pairs of position t at column t of idx/val (stride ld);
+ * mode 1 (resid): rest_sq[order[t]] = energy of the discarded coefficients,
+ * score[order[t]] (optional) = the kept score of `kind`.
+ * Workspace: sbo_round_i8_workspace_bytes(nblocks). */
+size_t sbo_round_i8_workspace_bytes(int nblocks);
+int sbo_round_i8_segments(const void* ydig, int sy, const int32_t* order,
+                          const int32_t* seg_block, const int64_t* seg_lo,
+                          const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
+                          const double* blocks, int nblocks, int block_override, int s0,
+                          int mode, int kind, int64_t ld, int16_t* idx, double* val,
+                          double* rest_sq, double* score, void* workspace, size_t ws_bytes,
+                          void* stream);
+
 /* Sparse outer products P = Y X^T per block on the tcgen05 tensor cores
  * (onb.py:127-134; north_star "grouped GEMM Y_j X_j^T"), p = 64, float32
  * signals: y (as the transposed digit tiles of sbo_y_tiles, built once per

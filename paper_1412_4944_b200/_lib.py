@@ -44,6 +44,9 @@ _SIGS = {
     "sbo_residual_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, P, P, P]),
     "sbo_round_code_segments": (I, [P, I, I, P, P, P, P, P, I64, P, I, I, I64, P, P, P]),
     "sbo_outer_i8_segments": (I, [P, I, P, P, P, P, I64, I, I, I64, P, P, I, I, P, P, SZ, P]),
+    "sbo_round_i8_workspace_bytes": (SZ, [I]),
+    "sbo_round_i8_segments": (I, [P, I, P, P, P, P, P, I64, P, I, I, I, I, I, I64, P, P, P, P,
+                                  P, SZ, P]),
     "sbo_y_tiles_bytes": (SZ, [I64, I64]),
     "sbo_y_tiles": (I, [P, P, P, P, P, I64, P, P]),
     "sbo_outer_i8_workspace_bytes": (SZ, [I]),

@@ -248,6 +248,7 @@ class Engine:
         bits (unit-range image patches do); otherwise the rounds run the fused
         float64 DMMA kernel."""
         self.i8 = None
+        self.ri8 = False
         if (self.p != 64 or self.sig.code != L.F32 or self.m == 0
                 or os.environ.get("SBO_I8", "1") != "1"):
             return
@@ -264,6 +265,8 @@ class Engine:
         xmax = math.sqrt(norm2) * (1.0 + 1e-6)  # |x| <= ||y|| (orthonormal blocks)
         ex = math.floor(math.log2(xmax)) + 1 if xmax > 0 else 0
         self.i8 = (sy, 54 - ex)
+        # the round's projection from the same digits (k <= 32 selection networks)
+        self.ri8 = self.k <= 32 and os.environ.get("SBO_RI8", "1") == "1"
         # signal-major digit rows (5 planes x 64 dims per signal), built once
         self.ydig = torch.empty((self.m, 5 * 64), dtype=torch.int8, device=self.dev)
         self._call("sbo_y_digits", self.sig.y.data_ptr(), self.sig.code, self.m, self.p, sy,
@@ -480,11 +483,22 @@ class Engine:
             if self.i8 is not None:
                 # coding (float64 DMMA projection, exact selection) writes the kept
                 # pairs; P = Y X^T on tcgen05 from exact integer digits
-                self._call("sbo_round_code_segments", self.sig.y.data_ptr(), self.sig.code, p,
-                           _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
-                           g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
-                           self.blocks.data_ptr(), override, self.s0, ld, idx.data_ptr(),
-                           val.data_ptr(), self.stream, units=n)
+                if self.ri8:
+                    # the projection on tcgen05 from exact integer digits
+                    nb = first_block + 1 if single else nblocks
+                    ws = self.scratch.get("ri8", L.size("sbo_round_i8_workspace_bytes", nb))
+                    self._call("sbo_round_i8_segments", self.ydig.data_ptr(), self.i8[0],
+                               _ptr(order), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
+                               g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
+                               self.blocks.data_ptr(), nb, override, self.s0, 0, self.kind,
+                               ld, idx.data_ptr(), val.data_ptr(), None, None, ws.data_ptr(),
+                               ws.numel(), self.stream, units=n)
+                else:
+                    self._call("sbo_round_code_segments", self.sig.y.data_ptr(),
+                               self.sig.code, p, _ptr(order), g.seg_block.data_ptr(),
+                               g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(),
+                               g.max_seg, self.blocks.data_ptr(), override, self.s0, ld,
+                               idx.data_ptr(), val.data_ptr(), self.stream, units=n)
                 self._call("sbo_outer_i8_segments", ytiles.data_ptr(), p,
                            None if single else g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
                            g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, nblocks,
@@ -571,7 +585,16 @@ class Engine:
             # float32-accurate, so recode every signal in its winning block in
             # float64 (exact support + discarded energy), as the worst set needs
             g = self.group(self.K)
-            if self.p <= 64:
+            if self.ri8:
+                ws = self.scratch.get("ri8", L.size("sbo_round_i8_workspace_bytes", self.K))
+                self._call("sbo_round_i8_segments", self.ydig.data_ptr(), self.i8[0],
+                           g.perm.data_ptr(), g.seg_block.data_ptr(), g.seg_lo.data_ptr(),
+                           g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg,
+                           self.blocks.data_ptr(), self.K, -1, self.s0, 1, self.kind, 0,
+                           None, None, self.state.residual.data_ptr(),
+                           self.state.score.data_ptr(), ws.data_ptr(), ws.numel(),
+                           self.stream, units=self.m)
+            elif self.p <= 64:
                 self._call("sbo_residual_segments", self.sig.y.data_ptr(), self.sig.code,
                            self.p, g.perm.data_ptr(), g.seg_block.data_ptr(),
                            g.seg_lo.data_ptr(), g.seg_hi.data_ptr(), g.nseg.data_ptr(),
