@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libsbo_b200.so"
+# SBO_LIB: an alternative in-tree build of the same library (A/B measurements)
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("SBO_LIB", "libsbo_b200.so")
 
 OK, EINVAL, ENUMERICAL, EDECOMP, ECUDA = 0, 1, 2, 3, 4
 KIND = {"squared-sum": 0, "abs-sum": 1}

@@ -55,29 +55,45 @@ constexpr int A_SLAB = TS * 128;        // 16 KB
 constexpr int A_BYTES = 3 * A_SLAB;     // 48 KB
 constexpr int B_SLAB = P * 128;         // 8 KB
 constexpr int B_BYTES = 4 * B_SLAB;     // 32 KB: the block's digit image
-constexpr int EPI_THREADS = 256;
-constexpr int MMA_WARP = 8;
-constexpr int PROD_WARP0 = 9, NPROD = 64;
-constexpr int THREADS = 352;
 constexpr int MODE_CODE = 0, MODE_RESID = 1;
-constexpr int GMAX = 32;
 
+// Role layout for NQ epilogue atom parts (NQ = 2: 32 atoms per thread, any
+// k <= 32; NQ = 4: 16 atoms per thread, k <= 16, twice the epilogue warps for
+// latency hiding): warps [0, 4 NQ) epilogue, then the MMA issuer, then the
+// producers.
+template <int NQ>
+struct Roles {
+  static constexpr int AQ = 64 / NQ;                 // atoms per epilogue thread
+  static constexpr int EPI_WARPS = 4 * NQ;
+  static constexpr int EPI_THREADS = 32 * EPI_WARPS;
+  static constexpr int MMA_WARP = EPI_WARPS;
+  static constexpr int PROD_WARP0 = EPI_WARPS + 1;
+  static constexpr int PROD_WARPS = 2;
+  static constexpr int NPROD = 32 * PROD_WARPS;
+  static constexpr int THREADS = 32 * (EPI_WARPS + 1 + PROD_WARPS);
+  static constexpr int GMAX = NQ == 2 ? 32 : 16;     // largest top-G list (k <= GMAX)
+};
+
+template <int NQ>
 struct Smem {
+  static constexpr int GMAX = Roles<NQ>::GMAX;
   int8_t a[2][A_BYTES];
   int8_t b[B_BYTES];
-  int32_t lists[2][GMAX][TS];   // [half][rank][row]: per-half top-G keys
-  int32_t cnt[2][2][TS];        // exchange buffers [parity][half][row]
-  double part[2][2][TS];        // [half][rest | score][row]
+  int32_t lists[NQ][GMAX][TS];  // [part][rank][row]: per-part top-G keys
+  int32_t cnt[2][NQ][TS];       // exchange buffers [parity][part][row]
+  double part[NQ][2][TS];       // [part][rest | score][row]
   int16_t oidx[GMAX][TS];       // code outputs staged per (slot, row)
   double oval[GMAX][TS];
   uint64_t full[2], empty[2], acc_full, acc_empty, b_full;
   uint32_t tmem;
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+template <int NQ>
+constexpr size_t smem_bytes() { return sizeof(Smem<NQ>) + 1024; }
 
-__device__ __forceinline__ Smem* smem_of(unsigned char* raw) {
+template <int NQ>
+__device__ __forceinline__ Smem<NQ>* smem_of(unsigned char* raw) {
   const uint32_t a = sm100::smem_u32(raw);
-  return reinterpret_cast<Smem*>(raw + ((1024u - (a & 1023u)) & 1023u));
+  return reinterpret_cast<Smem<NQ>*>(raw + ((1024u - (a & 1023u)) & 1023u));
 }
 
 __host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
@@ -127,16 +143,20 @@ struct Ring {
 
 __device__ __forceinline__ int sel_i(bool c, int a, int b) { return c ? a : b; }
 
-template <int G, int MODE>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int G, int MODE, int NQ>
+__global__ void __launch_bounds__(Roles<NQ>::THREADS, 1)
 k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
            const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
            const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg_p,
            const int8_t* __restrict__ qdig, int block_override, int k, int kind,
            double cscale, int64_t ld, int16_t* __restrict__ cidx, double* __restrict__ cval,
            double* __restrict__ rest_sq, double* __restrict__ score) {
+  using R = Roles<NQ>;
+  constexpr int AQ = R::AQ, EPI_THREADS = R::EPI_THREADS, MMA_WARP = R::MMA_WARP;
+  constexpr int PROD_WARP0 = R::PROD_WARP0, NPROD = R::NPROD;
+  static_assert(G <= R::GMAX, "top-G list longer than the part lists");
   extern __shared__ unsigned char raw[];
-  Smem* S = smem_of(raw);
+  Smem<NQ>* S = smem_of<NQ>(raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nseg = *nseg_p;
   if (tid == 0) {
@@ -159,10 +179,11 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
   auto block_of = [&](int seg) { return block_override >= 0 ? block_override : seg_block[seg]; };
 
   if (warp >= PROD_WARP0) {  // ------------------------------------------ producers
-    // warp pw gathers rows [64 pw, 64 pw + 64) of each tile, 8 rows (160 16-B
-    // chunks) per 5 copy rounds: lane l takes chunk q = l + 32 j of the group,
-    // row q / 20, chunk q % 20 (digit (q % 20) / 4).  The rows' signal ids are
-    // loaded before the stage wait (two per lane) and shuffled to the copies.
+    // producer warp pw gathers rows [RPW pw, RPW pw + RPW) of each tile, 8 rows
+    // (160 16-B chunks) per 5 copy rounds: lane l takes chunk q = l + 32 j of
+    // the group, row q / 20, chunk q % 20 (digit (q % 20) / 4).  The rows'
+    // signal ids are loaded before the stage wait and shuffled to the copies.
+    constexpr int RPW = TS / R::PROD_WARPS, OR = RPW / 32;
     const int pw = warp - PROD_WARP0;
     int rj[5], cj[5];
 #pragma unroll
@@ -176,19 +197,19 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
       const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
       for (int64_t t0 = lo; t0 < hi; t0 += TS) {
         const int n = static_cast<int>(min64(TS, hi - t0));
-        int o[2];
+        int o[OR];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = 64 * pw + 32 * h + lane;
+        for (int h = 0; h < OR; ++h) {
+          const int row = RPW * pw + 32 * h + lane;
           o[h] = row < n ? (order ? order[t0 + row] : static_cast<int>(t0 + row)) : 0;
         }
         sm100::mbar_wait(&S->empty[r.i], r.ph ^ 1u);
         const uint32_t base = sm100::smem_u32(S->a[r.i]);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
+        for (int g = 0; g < RPW / 8; ++g) {
 #pragma unroll
           for (int j = 0; j < 5; ++j) {
-            const int rl = 8 * g + rj[j], row = 64 * pw + rl;
+            const int rl = 8 * g + rj[j], row = RPW * pw + rl;
             const int sig = __shfl_sync(0xffffffffu, o[g >> 2], rl & 31);
             const int c = cj[j], a = c >> 2;
             cp_async16(base + (a >> 1) * A_SLAB + slab_off(row, (a & 1) * 64 + (c & 3) * 16),
@@ -261,12 +282,39 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
       }
     }
   } else {  // ------------------------------------------------------------ epilogue
-    const int q4 = warp & 3, half = warp >> 2;
+    const int q4 = warp & 3, part = warp >> 2;
     const int row = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q4) << 16);
-    const int a0 = 32 * half;  // this thread's atoms [a0, a0 + 32)
+    const int a0 = AQ * part;  // this thread's atoms [a0, a0 + AQ)
     int xb = 0;  // exchange buffer parity
     uint32_t acc_ph = 0;
+    auto bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(EPI_THREADS) : "memory"); };
+    auto any_of = [&](bool pr) {
+      int r;
+      asm volatile(
+          "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
+          "bar.red.or.pred q, 2, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+          : "=r"(r)
+          : "r"(static_cast<int>(pr)), "r"(EPI_THREADS)
+          : "memory");
+      return r != 0;
+    };
+    // the row's per-part values (a barrier: called by every epilogue thread);
+    // returns the total and, in `before`, the sum over the parts below this one
+    auto gather = [&](int mine, int& before) {
+      S->cnt[xb][part][row] = mine;
+      bar();
+      int tot = 0;
+      before = 0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int x = S->cnt[xb][q][row];
+        tot += x;
+        before += q < part ? x : 0;
+      }
+      xb ^= 1;
+      return tot;
+    };
     for (int seg = sa; seg < sb; ++seg) {
       const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
       for (int64_t t0 = lo; t0 < hi; t0 += TS) {
@@ -277,11 +325,11 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         sm100::mbar_wait(&S->acc_full, acc_ph);
         acc_ph ^= 1u;
         sm100::tc_fence_after();
-        double c[32];
+        double c[AQ];
         // selection key of atom a0 + i: the high word of |c| (-1: inactive row)
         auto key = [&](int i) { return act ? (__double2hiint(c[i]) & 0x7FFFFFFF) : -1; };
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < AQ / 8; ++q) {
           uint32_t v[8][8];  // [level][atom]: 8 atoms per TMEM round trip
 #pragma unroll
           for (int L = 0; L < 8; ++L) {
@@ -310,44 +358,37 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         if (lane == 0) sm100::mbar_arrive(&S->acc_empty);  // TMEM free for the next tile
 
         // ---- selection (select_top, onb.py:58-76): the k-th largest key over
-        // both halves; exactly k keys at or above it -> the kept set
-        auto bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(EPI_THREADS) : "memory"); };
-        auto any_of = [&](bool pr) {
-          int r;
-          asm volatile(
-              "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
-              "bar.red.or.pred q, 2, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
-              : "=r"(r)
-              : "r"(static_cast<int>(pr)), "r"(EPI_THREADS)
-              : "memory");
-          return r != 0;
-        };
-        // the partner thread's (other half, same row) value; alternating buffers
-        auto exch = [&](int mine) {
-          S->cnt[xb][half][row] = mine;
-          bar();
-          const int o = S->cnt[xb][half ^ 1][row];
-          xb ^= 1;
-          return o;
-        };
-        // kk-th largest of the row's 64 keys (kk <= G): per-half top-G lists merged
+        // the row's parts; exactly k keys at or above it -> the kept set.
+        // kk-th largest of the row's 64 keys (kk <= G): per-part top-G lists
+        // merged through shared memory
         auto kth = [&](auto keyf, int kk) {
-          int v[32];
+          int v[AQ >= G ? AQ : G];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = keyf(i);
+          for (int i = 0; i < AQ; ++i) v[i] = keyf(i);
 #pragma unroll
-          for (int g = 0; g < 32; g += G) topk::sort_desc<G>(v + g);
+          for (int i = AQ; i < G; ++i) v[i] = static_cast<int>(0x80000000u);
+          constexpr int W = AQ >= G ? G : AQ;  // sorted run length
+          if constexpr (AQ >= G) {
 #pragma unroll
-          for (int step = G; step < 32; step <<= 1) {
+            for (int g = 0; g < AQ; g += G) topk::sort_desc<G>(v + g);
 #pragma unroll
-            for (int g = 0; g + step < 32; g += 2 * step) topk::merge_top<G>(v + g, v + g + step);
+            for (int step = G; step < AQ; step <<= 1) {
+#pragma unroll
+              for (int g = 0; g + step < AQ; g += 2 * step) topk::merge_top<G>(v + g, v + g + step);
+            }
+          } else {
+            topk::sort_desc<W>(v);  // the whole part (padding stays at the end)
           }
 #pragma unroll
-          for (int i = 0; i < G; ++i) S->lists[half][i][row] = v[i];
+          for (int i = 0; i < G; ++i) S->lists[part][i][row] = v[i];
           bar();
 #pragma unroll
-          for (int i = 0; i < G; ++i) v[i] = topk::vmax(v[i], S->lists[half ^ 1][G - 1 - i][row]);
-          topk::merge_desc<G>(v);
+          for (int q = 1; q < NQ; ++q) {
+            const int o = (part + q) % NQ;
+#pragma unroll
+            for (int i = 0; i < G; ++i) v[i] = topk::vmax(v[i], S->lists[o][G - 1 - i][row]);
+            topk::merge_desc<G>(v);
+          }
           int t = v[0];
 #pragma unroll
           for (int i = 1; i < G; ++i) t = sel_i(i == kk - 1, v[i], t);
@@ -356,24 +397,24 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         const int t1 = kth(key, k);
         uint32_t mask = 0u;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
+        for (int i = 0; i < AQ; ++i)
           if (key(i) >= t1 && key(i) >= 0) mask |= 1u << i;
-        int nlow = __popc(mask);
-        const int other1 = exch(nlow);
-        if (half) nlow = other1;
-        const bool need = act && nlow + (half ? __popc(mask) : other1) != k;
+        int before;
+        const int kept_all = gather(__popc(mask), before);  // (unconditional: a barrier)
+        const bool need = act && kept_all != k;
         if (any_of(need)) {
           // a key tie at the threshold (a 2^-20 relative gap): the tied atoms
           // are ordered by the low word of |c| (the full float64 magnitude),
-          // then, for equal magnitudes, by atom (stable argsort: lower first)
+          // then, for equal magnitudes, by atom (stable argsort: lower first).
+          // Every gather is a barrier: called unconditionally by all threads.
           uint32_t gt1 = 0u, tie = 0u;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < AQ; ++i) {
             gt1 |= (key(i) > t1 ? 1u : 0u) << i;
             tie |= (key(i) == t1 ? 1u : 0u) << i;
           }
-          // (every exchange is a barrier: called unconditionally by all 256 threads)
-          const int gt1_all = __popc(gt1) + exch(__popc(gt1));
+          int dummy;
+          const int gt1_all = gather(__popc(gt1), dummy);
           const int r = need ? k - gt1_all : 1;
           auto key2 = [&](int i) {
             return need && ((tie >> i) & 1u)
@@ -383,20 +424,20 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
           const int t2 = kth(key2, r);
           uint32_t ge2 = 0u, gt2 = 0u;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < AQ; ++i) {
             ge2 |= (((tie >> i) & 1u) && key2(i) >= t2 ? 1u : 0u) << i;
             gt2 |= (((tie >> i) & 1u) && key2(i) > t2 ? 1u : 0u) << i;
           }
-          const int ge2_all = __popc(ge2) + exch(__popc(ge2));
+          const int ge2_all = gather(__popc(ge2), dummy);
           const bool need3 = need && ge2_all != r;
           uint32_t take = ge2;
           if (any_of(need3)) {
             // equal float64 magnitudes at the threshold: the lowest atoms first
-            const int nd = r - (__popc(gt2) + exch(__popc(gt2)));
+            const int nd = r - gather(__popc(gt2), dummy);
             const uint32_t eq = ge2 & ~gt2;
-            const int eq_lo = exch(half ? 0 : __popc(eq));
-            const int low_takes = min(nd, half ? eq_lo : __popc(eq));
-            int mine = half ? nd - low_takes : low_takes;
+            int eq_before;
+            gather(__popc(eq), eq_before);
+            int mine = min(max(nd - eq_before, 0), __popc(eq));
             if (need3) {
               take = gt2;
               uint32_t e = eq;
@@ -407,17 +448,18 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
             }
           }
           if (need) mask = gt1 | take;
-          const int lo_cnt = exch(half ? 0 : __popc(mask));
-          if (need) nlow = half ? lo_cnt : __popc(mask);
+          int b2;
+          gather(__popc(mask), b2);
+          if (need) before = b2;
         }
         // ---- outputs
         if constexpr (MODE == MODE_CODE) {
           // the kept pairs in ascending atom order, staged per (slot, row) in
           // shared memory, then written as coalesced rows of the code matrices
           if (act) {
-            int at = half ? nlow : 0;
+            int at = before;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < AQ; ++i) {
               if ((mask >> i) & 1u) {
                 S->oidx[at][row] = static_cast<int16_t>(a0 + i);
                 S->oval[at][row] = c[i];
@@ -435,22 +477,29 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
             }
           }
         } else {
-          // discarded energy (no kept-sum cancellation) and the kept score
+          // discarded energy (no kept-sum cancellation) and the kept score,
+          // summed over the parts in a fixed order
           double rest = 0.0, sc = 0.0;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < AQ; ++i) {
             const double x = c[i];
             if ((mask >> i) & 1u) sc = kind == SBO_KIND_SQUARED_SUM ? fma(x, x, sc) : sc + fabs(x);
             else rest = fma(x, x, rest);
           }
-          S->part[half][0][row] = rest;
-          S->part[half][1][row] = sc;
-          asm volatile("bar.sync 1, %0;" ::"r"(EPI_THREADS) : "memory");
-          if (half == 0 && act) {
-            rest_sq[sig] = S->part[0][0][row] + S->part[1][0][row];
-            if (score) score[sig] = S->part[0][1][row] + S->part[1][1][row];
+          S->part[part][0][row] = rest;
+          S->part[part][1][row] = sc;
+          bar();
+          if (part == 0 && act) {
+            double rs = 0.0, ss = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              rs += S->part[q][0][row];
+              ss += S->part[q][1][row];
+            }
+            rest_sq[sig] = rs;
+            if (score) score[sig] = ss;
           }
-          asm volatile("bar.sync 1, %0;" ::"r"(EPI_THREADS) : "memory");
+          bar();
         }
       }
     }
@@ -484,24 +533,29 @@ __global__ void k_q_digits(const double* __restrict__ blocks, int b0, int nb,
 
 using namespace sbo;
 
+#ifndef RI8_NQ
+#define RI8_NQ 2  // epilogue atom parts for s0 <= 16 (4 parts, 16 epilogue warps: measured slower, 25.5 vs 22.8 ms per config-C iteration)
+#endif
+
 extern "C" size_t sbo_round_i8_workspace_bytes(int nblocks) {
   return static_cast<size_t>(nblocks > 0 ? nblocks : 0) * ri8::B_BYTES;
 }
 
-template <int G, int MODE>
+template <int G, int MODE, int NQ>
 static int launch_ri8(unsigned grid, cudaStream_t st, const int8_t* ydig, const int32_t* order,
                       const int32_t* seg_block, const int64_t* seg_lo, const int64_t* seg_hi,
                       const int32_t* nseg, const int8_t* qdig, int ov, int k, int kind,
                       double cscale, int64_t ld, int16_t* idx, double* val, double* rest_sq,
                       double* score) {
   static bool attr = false;
+  constexpr size_t smem = ri8::smem_bytes<NQ>();
   if (!attr) {
-    SBO_CHECK_CUDA(cudaFuncSetAttribute(ri8::k_round_i8<G, MODE>,
+    SBO_CHECK_CUDA(cudaFuncSetAttribute(ri8::k_round_i8<G, MODE, NQ>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ri8::SMEM_BYTES)));
+                                        static_cast<int>(smem)));
     attr = true;
   }
-  ri8::k_round_i8<G, MODE><<<grid, ri8::THREADS, ri8::SMEM_BYTES, st>>>(
+  ri8::k_round_i8<G, MODE, NQ><<<grid, ri8::Roles<NQ>::THREADS, smem, st>>>(
       ydig, order, seg_block, seg_lo, seg_hi, nseg, qdig, ov, k, kind, cscale, ld, idx, val,
       rest_sq, score);
   return check_launch(MODE == ri8::MODE_CODE ? "k_round_i8<code>" : "k_round_i8<resid>");
@@ -537,16 +591,16 @@ extern "C" int sbo_round_i8_segments(const void* ydig, int sy, const int32_t* or
   const unsigned grid = static_cast<unsigned>(min64(max_seg, sms));
   const double cscale = ldexp(1.0, -sy - 26);
   const auto* yd = static_cast<const int8_t*>(ydig);
-#define RI8_GO(G_)                                                                            \
+#define RI8_GO(G_, NQ_)                                                                       \
   return mode == ri8::MODE_CODE                                                                \
-             ? launch_ri8<G_, ri8::MODE_CODE>(grid, st, yd, order, seg_block, seg_lo, seg_hi,  \
+             ? launch_ri8<G_, ri8::MODE_CODE, NQ_>(grid, st, yd, order, seg_block, seg_lo, seg_hi,  \
                                               nseg, qdig, block_override, s0, kind, cscale,     \
                                               ld, idx, val, rest_sq, score)               \
-             : launch_ri8<G_, ri8::MODE_RESID>(grid, st, yd, order, seg_block, seg_lo, seg_hi, \
+             : launch_ri8<G_, ri8::MODE_RESID, NQ_>(grid, st, yd, order, seg_block, seg_lo, seg_hi, \
                                                nseg, qdig, block_override, s0, kind, cscale,    \
                                                ld, idx, val, rest_sq, score)
-  if (s0 <= 8) RI8_GO(8);
-  if (s0 <= 16) RI8_GO(16);
-  RI8_GO(32);
+  if (s0 <= 8) RI8_GO(8, RI8_NQ);
+  if (s0 <= 16) RI8_GO(16, RI8_NQ);
+  RI8_GO(32, 2);
 #undef RI8_GO
 }
