@@ -326,8 +326,9 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         acc_ph ^= 1u;
         sm100::tc_fence_after();
         double c[AQ];
-        // selection key of atom a0 + i: the high word of |c| (-1: inactive row)
-        auto key = [&](int i) { return act ? (__double2hiint(c[i]) & 0x7FFFFFFF) : -1; };
+        // selection key of atom a0 + i: the high word of |c| (an inactive row's
+        // keys are garbage: its outputs are never written)
+        auto key = [&](int i) { return __double2hiint(c[i]) & 0x7FFFFFFF; };
 #pragma unroll
         for (int q = 0; q < AQ / 8; ++q) {
           uint32_t v[8][8];  // [level][atom]: 8 atoms per TMEM round trip
@@ -398,7 +399,7 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         uint32_t mask = 0u;
 #pragma unroll
         for (int i = 0; i < AQ; ++i)
-          if (key(i) >= t1 && key(i) >= 0) mask |= 1u << i;
+          if (key(i) >= t1) mask |= 1u << i;
         int before;
         const int kept_all = gather(__popc(mask), before);  // (unconditional: a barrier)
         const bool need = act && kept_all != k;
