@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--m", dest="m_total", type=int, default=1 << 24,
+    # (not "--m": torch.distributed.run rejects it as an ambiguous prefix when
+    # --gpus N re-launches this script)
+    ap.add_argument("--m-total", dest="m_total", type=int, default=1 << 24,
                     help="signals in the whole job (config C: 2^24)")
     ap.add_argument("--m-per-gpu", dest="m_per_gpu", type=int, default=None,
                     help="weak scaling: signals per GPU (overrides --m)")
@@ -166,6 +168,7 @@ def peaks():
 #   code   (sbo_code_segments, unit = signal): projection 2p^2
 FP64_PEAK_TFLOPS = 33.0       # measured DFMA throughput on this pool (profiles/fp64_micro.txt)
 DMMA_PEAK_TFLOPS = 37.0       # measured float64 tensor-core (DMMA m8n8k4) throughput, same file
+I8_PEAK_TOPS = 4188.7         # measured tcgen05 kind::i8 dense throughput (profiles/i8_micro.txt)
 
 
 def kernel_families(timer, p, k):
@@ -177,6 +180,9 @@ def kernel_families(timer, p, k):
            "sbo_tc_energy": ("k_energy_tc", 2 * p * p, 6 * p * p, "tcgen05 split-fp16"),
            "sbo_round_code_segments": ("k_round64<code>", 2 * p * p, 2 * p * p,
                                        "fp64 tensor cores (DMMA)"),
+           # 1920 digit-product columns x 64 dims x 2 int8 ops per signal (round_i8.cu)
+           "sbo_round_i8_segments": ("k_round_i8", 2 * p * p, 2 * 64 * 1920,
+                                     "tcgen05 kind::i8 (exact integer digits)"),
            # 1280 digit-product columns x 128 rows x 2 int8 ops per signal (outer_i8.cu)
            "sbo_outer_i8_segments": ("k_outer_i8", 2 * p * k, 2 * 128 * 1280,
                                      "tcgen05 kind::i8 (exact integer digits)"),
@@ -208,7 +214,8 @@ def ncu_traffic(kname):
     import glob
     files = sorted(glob.glob(str(ROOT / "profiles" / "*_ncu_summary.txt")))
     want = {"k_round64": "k_round64<float, 0>", "k_round64<resid>": "k_round64<float, 1>",
-            "k_energy_tc": "k_energy_tc<"}.get(kname)
+            "k_energy_tc": "k_energy_tc<", "k_round_i8": "k_round_i8<",
+            "k_outer_i8": "k_outer_i8"}.get(kname)
     if not files or not want:
         return None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -239,11 +246,19 @@ def roofline_of(kname, info, bf16, src, steps):
             "dmma_peak": DMMA_PEAK_TFLOPS,
             "frac_of_dmma_peak": achieved / DMMA_PEAK_TFLOPS if "DMMA" in info["pipe"] else None,
             "implemented_tflops": info.get("implemented_tflops"),
+            "i8_peak_tops": I8_PEAK_TOPS if "i8" in info["pipe"] else None,
+            "implemented_frac_of_i8_peak": (info["implemented_tflops"] / I8_PEAK_TOPS
+                                            if "i8" in info["pipe"]
+                                            and info.get("implemented_tflops") else None),
             "implemented_frac_of_dmma_peak": (info["implemented_tflops"] / DMMA_PEAK_TFLOPS
                                               if "DMMA" in info["pipe"]
                                               and info.get("implemented_tflops") else None),
             "note": ("float64 kernel: the bf16 tensor peak is not its ceiling; the measured "
-                     "float64 tensor-core (DMMA) peak is" if "fp64" in info["pipe"] else None),
+                     "float64 tensor-core (DMMA) peak is" if "fp64" in info["pipe"] else
+                     "float64-exact projection from int8 digits: `achieved` counts the "
+                     "reference's 2p^2 flop per signal; the int8 ops it issues "
+                     "(implemented_tflops, in TOPS) are rated against the measured kind::i8 "
+                     "peak" if "i8" in info["pipe"] else None),
             "pipe": info["pipe"], "launches_per_step": info["launches"] / steps,
             "ms_per_step": info["ms_total"] / steps,
             "algorithmic": f"{info['flop_per_unit']} flop per unit, {info['units'] // steps} "
@@ -336,7 +351,8 @@ KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1
                     "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_sum": 2,
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2,
                     "sbo_round_code_segments": 1, "sbo_outer_i8_segments": 1, "sbo_i8_scan": 1,
-                    "sbo_y_digits": 1, "sbo_y_tiles": 1}
+                    "sbo_y_digits": 1, "sbo_y_tiles": 1, "sbo_round_i8_segments": 2,
+                    "sbo_gram_counted": 3, "sbo_chunk_segments": 1}
 
 
 def max_over_ranks(x: float, dist, dev) -> float:
@@ -412,13 +428,20 @@ def run_ours(a):
     for _ in range(a.warmup):
         restore()
         eng.iterate(w, a.rounds, draws)
-    # one GPU: the step (restore + iteration) is replayed as a CUDA graph, which
-    # removes the host launch gaps; the sharded path runs eagerly (host exchanges)
-    use_graph = world == 1 and os.environ.get("SBO_BENCH_NO_GRAPH", "0") != "1"
-    replay = None
+    # the step (restore + iteration) is replayed as a CUDA graph, which removes the
+    # host launch gaps: on one GPU, and sharded over NCCL (stream-ordered
+    # collectives, member counts kept on the device); gloo runs eagerly
+    use_graph = ((world == 1 or getattr(comm, "capturable", False))
+                 and os.environ.get("SBO_BENCH_NO_GRAPH", "0") != "1")
+    replay, graph_note = None, None
     if use_graph:
         draws_dev = torch.from_numpy(np.ascontiguousarray(draws)).to(dev)
-        replay = eng.capture_iteration(entering, w, a.rounds, draws_dev)
+        try:
+            replay = eng.capture_iteration(entering, w, a.rounds, draws_dev)
+        except Exception as e:  # eager steps instead; the line says why
+            graph_note = f"capture failed, eager steps: {type(e).__name__}: {e}"[:300]
+            replay = None
+            torch.cuda.synchronize()
     # kernels of one step (ABI calls x kernels per call), counted on an eager step
     calls = {}
     orig = eng._call
@@ -511,6 +534,7 @@ def run_ours(a):
         "clocks": clocks,
         "gpu_launches": launches,
         "cuda_graph": bool(replay is not None),
+        "cuda_graph_note": graph_note,
         "phases_ms": {"worst+new_block": phases[0], "represent1": phases[1],
                       "group+retrain": phases[2], "represent2": phases[3]},
         "roofline": roofline_of(dom[0], dom[1], bf16, src, steps=a.steps),

@@ -276,6 +276,16 @@ int sbo_residual_segments(const void* y, int dtype, int p, const int32_t* order,
 size_t sbo_gram_workspace_bytes(int64_t w, int chunk, int p);
 int sbo_gram(const void* y, int dtype, int p, const int32_t* members, int64_t w, int chunk,
              double* G, void* ws, size_t ws_bytes, void* stream);
+/* sbo_gram over the first min(w, *count) members, count read on the device (a
+ * sharded worst set's local member count stays in device memory; w sizes the
+ * workspace and launches). */
+int sbo_gram_counted(const void* y, int dtype, int p, const int32_t* members, int64_t w,
+                     const int64_t* count, int chunk, double* G, void* ws, size_t ws_bytes,
+                     void* stream);
+/* Segment table of a list of min(w, *count) entries (count NULL: w) in chunks
+ * of `chunk`: seg_lo/seg_hi (ceil(w / chunk) entries), *nseg = the used count. */
+int sbo_chunk_segments(int64_t w, const int64_t* count, int chunk, int64_t* seg_lo,
+                       int64_t* seg_hi, int32_t* nseg, void* stream);
 
 /* select_top on explicit float64 coefficient vectors (onb.py:58-76): vector j
  * is row j of coeffs (t x p); codes written at column j (row stride ld). */

@@ -55,6 +55,8 @@ _SIGS = {
     "sbo_y_digits": (I, [P, I, I64, I, I, P, P]),
     "sbo_gram_workspace_bytes": (SZ, [I64, I, I]),
     "sbo_gram": (I, [P, I, I, P, I64, I, P, P, SZ, P]),
+    "sbo_gram_counted": (I, [P, I, I, P, I64, P, I, P, P, SZ, P]),
+    "sbo_chunk_segments": (I, [I64, P, I, P, P, P, P]),
     "sbo_select_top": (I, [P, I64, I, I, I64, P, P, P]),
     "sbo_polar_workspace_bytes": (SZ, [I, I]),
     "sbo_polar": (I, [P, I, I, P, P, P, P, P, P, SZ, P]),

@@ -591,7 +591,11 @@ __global__ void __launch_bounds__(256) k_reduce_segments(const double* __restric
 }
 
 // Gram partials over chunks of a member list, then the ordered reduction
-__global__ void k_chunk_segments(int64_t w, int chunk, int64_t* lo, int64_t* hi, int32_t* nseg) {
+// (count, optional: the list length on the device, at most w — a sharded
+// worst set's local member count, never read back to the host)
+__global__ void k_chunk_segments(int64_t w, const int64_t* count, int chunk, int64_t* lo,
+                                 int64_t* hi, int32_t* nseg) {
+  if (count) w = min64(w, max(*count, int64_t(0)));
   const int64_t n = ceil_div(w, chunk);
   for (int64_t s = threadIdx.x; s < n; s += blockDim.x) {
     lo[s] = s * chunk;
@@ -760,8 +764,9 @@ extern "C" size_t sbo_gram_workspace_bytes(int64_t w, int chunk, int p) {
   return sizeof(double) * n * p * p + sizeof(int64_t) * 2 * n + 64;
 }
 
-extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members, int64_t w,
-                        int chunk, double* G, void* ws, size_t ws_bytes, void* stream) {
+extern "C" int sbo_gram_counted(const void* y, int dtype, int p, const int32_t* members,
+                                int64_t w, const int64_t* count, int chunk, double* G, void* ws,
+                                size_t ws_bytes, void* stream) {
   if (int rc = check_common(dtype, p, 1)) return rc;
   if (chunk < kTile || chunk % kTile) return fail(SBO_EINVAL, "chunk must be a multiple of 64");
   if (ws_bytes < sbo_gram_workspace_bytes(w, chunk, p))
@@ -776,7 +781,7 @@ extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members,
   int64_t* lo = reinterpret_cast<int64_t*>(partial + n * p * p);
   int64_t* hi = lo + n;
   int32_t* ns = reinterpret_cast<int32_t*>(hi + n);
-  k_chunk_segments<<<1, 256, 0, st>>>(w, chunk, lo, hi, ns);
+  k_chunk_segments<<<1, 256, 0, st>>>(w, count, chunk, lo, hi, ns);
   int rc = p <= 64 ? sbo_gram_partials64(y, dtype, p, members, lo, hi, ns, n, partial, st)
            : dtype == SBO_F32 ? outer_impl<float>(y, p, members, lo, hi, ns, n, 1, 0, nullptr,
                                                   nullptr, 1, partial, st)
@@ -787,6 +792,19 @@ extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members,
   k_reduce_segments<<<dim3(static_cast<unsigned>(ceil_div(pp, 32)), 1), 256, 0, st>>>(
       partial, nullptr, ns, 1, p, G);
   return check_launch("k_reduce_segments(gram)");
+}
+
+extern "C" int sbo_gram(const void* y, int dtype, int p, const int32_t* members, int64_t w,
+                        int chunk, double* G, void* ws, size_t ws_bytes, void* stream) {
+  return sbo_gram_counted(y, dtype, p, members, w, nullptr, chunk, G, ws, ws_bytes, stream);
+}
+
+extern "C" int sbo_chunk_segments(int64_t w, const int64_t* count, int chunk, int64_t* seg_lo,
+                                  int64_t* seg_hi, int32_t* nseg, void* stream) {
+  if (chunk < 1 || !seg_lo || !seg_hi || !nseg) return fail(SBO_EINVAL, "bad arguments");
+  k_chunk_segments<<<1, 256, 0, as_stream(stream)>>>(w > 0 ? w : 0, count, chunk, seg_lo,
+                                                     seg_hi, nseg);
+  return check_launch("k_chunk_segments");
 }
 
 // select_top on explicit float64 coefficients (onb.py:58-76): coefficient

@@ -64,6 +64,8 @@ class TorchComm(Comm):
         self.dist, self.group = dist, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        # NCCL collectives are stream-ordered device work (CUDA-graph capturable)
+        self.capturable = dist.get_backend(group) == "nccl"
 
     def allreduce(self, t):
         if t.is_cuda and self.dist.get_backend(self.group) != "nccl":
@@ -432,9 +434,20 @@ class Engine:
                    ws.numel(), self.stream)
         return g
 
-    def list_segments(self, n: int) -> Groups:
-        """Segment table of a single list of n entries (a member list)."""
+    def list_segments(self, n: int, count: torch.Tensor | None = None) -> Groups:
+        """Segment table of a single list of n entries (a member list); with
+        ``count`` (int64 device tensor), of its first min(n, count) entries,
+        built on the device (no host read of the count)."""
         sl = seg_len(n)
+        if count is not None:
+            max_seg = max(1, math.ceil(n / sl))
+            g = Groups(None, None, torch.zeros(max_seg, dtype=torch.int32, device=self.dev),
+                       torch.empty(max_seg, dtype=torch.int64, device=self.dev),
+                       torch.empty(max_seg, dtype=torch.int64, device=self.dev),
+                       torch.zeros(1, dtype=torch.int32, device=self.dev), max_seg)
+            self._call("sbo_chunk_segments", n, count.data_ptr(), sl, g.seg_lo.data_ptr(),
+                       g.seg_hi.data_ptr(), g.nseg.data_ptr(), self.stream)
+            return g
         nseg = max(1, math.ceil(n / sl)) if n > 0 else 0
         lo = torch.arange(0, max(n, 1), sl, dtype=torch.int64, device=self.dev)[:nseg]
         hi = torch.clamp(lo + sl, max=n)
@@ -527,12 +540,13 @@ class Engine:
                        status[r].data_ptr(), pol_ws.data_ptr(), pol_ws.numel(), self.stream,
                        units=nblocks)
 
-    def gram(self, members, w: int) -> torch.Tensor:
+    def gram(self, members, w: int, count: torch.Tensor | None = None) -> torch.Tensor:
         G = torch.empty((self.p, self.p), dtype=torch.float64, device=self.dev)
         chunk = seg_len(w)
         ws = self.scratch.get("gram", L.size("sbo_gram_workspace_bytes", w, chunk, self.p))
-        self._call("sbo_gram", self.sig.y.data_ptr(), self.sig.code, self.p, _ptr(members), w,
-                   chunk, G.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
+        self._call("sbo_gram_counted", self.sig.y.data_ptr(), self.sig.code, self.p,
+                   _ptr(members), w, _ptr(count), chunk, G.data_ptr(), ws.data_ptr(),
+                   ws.numel(), self.stream)
         return G
 
     def init_block(self, G, ncols: int, draws: np.ndarray, slot: int, status, rank=None):
@@ -564,8 +578,10 @@ class Engine:
                    self.block_ptr(slot), _ptr(rank), status.data_ptr(), ws.data_ptr(),
                    ws.numel(), self.stream)
 
-    def worst(self, w: int) -> tuple[torch.Tensor, int]:
-        """Local members of the global worst-w set (ascending signal order)."""
+    def worst(self, w: int) -> tuple[torch.Tensor, int, torch.Tensor | None]:
+        """Local members of the global worst-w set (ascending signal order):
+        (members, n, count).  One GPU: n members.  Sharded: at most n members,
+        the local count in the device tensor ``count`` (never read back here)."""
         res = self.state.residual
         if self.comm.world == 1:
             n = min(w, self.m)
@@ -573,7 +589,7 @@ class Engine:
             ws = self.scratch.get("worst", L.size("sbo_worst_workspace_bytes", self.m))
             self._call("sbo_worst_set", res.data_ptr(), self.m, w, members.data_ptr(),
                        ws.data_ptr(), ws.numel(), self.stream)
-            return members, n
+            return members, n, None
         return distributed_worst(self, w)
 
     # ----------------------------------------------------------- iteration
@@ -634,12 +650,12 @@ class Engine:
         self.reset_rotation(K0, K0 + 1)
         st = torch.zeros((2, rounds + 1, K0 + 1), dtype=torch.int32, device=self.dev)
         # worst set and the new block (sbo.py:353-357)
-        members, n = self.worst(w)
+        members, n, count = self.worst(w)
         if force_new_block is None:
             n_total = min(w, self.m_total)
-            G = self.comm.allreduce(self.gram(members, n))
+            G = self.comm.allreduce(self.gram(members, n, count))
             self.init_block(G, n_total, draws, K0, st[0, rounds, :1])
-            segs = self.list_segments(n)
+            segs = self.list_segments(n, count)
             self.train_rounds(members, segs, n, rounds, 1, K0, None, st[0], single=True)
         else:
             self.blocks[K0].copy_(torch.as_tensor(force_new_block, dtype=torch.float64))
@@ -658,7 +674,8 @@ class Engine:
         # represent #2 (sbo.py:389-394)
         self.represent_full()
         mark()
-        return {"status": st, "counts": counts, "members": members, "n": n, "K": self.K}
+        return {"status": st, "counts": counts, "members": members, "n": n, "count": count,
+                "K": self.K}
 
     def finish_iteration(self, d: dict) -> IterationOut:
         """Host side of an iteration: RMSE, status checks, empty-block list."""
@@ -670,7 +687,8 @@ class Engine:
         self.last_sweeps = (stc >> 8) & 0xFF
         check_status(stc, self.p)
         empty = [b for b in range(self.K) if cnt[b] == 0]
-        return IterationOut(self.K, rmse, empty, d["members"][: d["n"]])
+        n = d["n"] if d.get("count") is None else int(d["count"].item())
+        return IterationOut(self.K, rmse, empty, d["members"][:n])
 
     def capture(self, fn, prepare):
         """CUDA graph of ``fn()`` (device work only) after two eager warm-up runs on a
@@ -697,8 +715,9 @@ class Engine:
         repeated iterations from the same entering state on one GPU (the bench):
         replaying it removes the host launch gaps between the ~100 kernels.
         Returns replay() -> IterationOut."""
-        if self.comm.world > 1:
-            raise ValueError("graph capture is single-GPU (the sharded path has host exchanges)")
+        if self.comm.world > 1 and not getattr(self.comm, "capturable", False):
+            raise ValueError("graph capture of a sharded iteration needs NCCL collectives "
+                             "(gloo exchanges go through the host)")
         side = torch.cuda.Stream(self.dev)
         side.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(side):  # warm-up: scratch sizes, kernel attributes
@@ -734,20 +753,23 @@ def check_status(st: np.ndarray, p: int | None = None):
         raise NumericalError("block lost orthonormality: defect > 1e-08")
 
 
-def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int]:
+def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int, torch.Tensor]:
     """Global worst-w across ranks: radix select with allreduced 256-bin histograms.
 
     Keys are the float64 bit patterns of residual_sq (order-preserving for >= 0);
     ties at the threshold go to the lowest GLOBAL signal index, i.e. to lower
     ranks first (contiguous column shards) — dist.equal_quota's rule, applied on
     the device.  The select state, the eight histograms and the tie counts stay in
-    device memory (collectives stream-ordered on NCCL); the one host read is the
-    local member count, which sizes the Gram and segment launches."""
+    device memory (collectives stream-ordered on NCCL), and so does the local
+    member count: the Gram and the segment table read it on the device, launches
+    are sized by the bound min(w, m_local) — no host synchronisation, so the
+    sharded iteration can be captured as a CUDA graph on NCCL."""
     res = eng.state.residual
     need = min(w, eng.m_total)
     members = torch.empty(max(eng.m, 1), dtype=torch.int32, device=eng.dev)
+    count = torch.zeros(1, dtype=torch.int64, device=eng.dev)
     if need < 1:
-        return members, 0
+        return members, 0, count
     ws = eng.scratch.get("worst", L.size("sbo_worst_workspace_bytes", eng.m))
     hist = torch.empty(256, dtype=torch.int64, device=eng.dev)
     eng._call("sbo_select_begin", ws.data_ptr(), need, eng.stream)
@@ -760,8 +782,7 @@ def distributed_worst(eng: Engine, w: int) -> tuple[torch.Tensor, int]:
     eng._call("sbo_select_counts", res.data_ptr(), eng.m, ws.data_ptr(), ws.numel(),
               gt_eq.data_ptr(), eng.stream)
     eq_all = eng.comm.allgather(gt_eq[1:2].clone())
-    count = torch.empty(1, dtype=torch.int64, device=eng.dev)
     eng._call("sbo_select_write", res.data_ptr(), eng.m, ws.data_ptr(), ws.numel(),
               gt_eq.data_ptr(), eq_all.data_ptr(), eng.comm.rank, members.data_ptr(),
               count.data_ptr(), eng.stream)
-    return members, int(count.item())
+    return members, min(need, eng.m), count

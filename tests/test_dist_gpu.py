@@ -22,16 +22,19 @@ def _free_port():
     return port
 
 
-def _problem():
+def _problem(kind="gaussian"):
+    """Gaussian rows (the float64 DMMA rounds) or unit-range patches (the
+    integer-digit tcgen05 rounds, round_i8.cu / outer_i8.cu)."""
     from paper_1412_4944_b200 import signals
     rng = np.random.default_rng(77)
     p, K = 64, 4
-    y32 = signals.gaussian_signals(p, 16384, seed=9)
+    y32 = (signals.gaussian_signals(p, 16384, seed=9) if kind == "gaussian"
+           else signals.patch_signals(16384, 8, 512, 512))
     blocks = np.stack([np.linalg.qr(rng.standard_normal((p, p)))[0] for _ in range(K)])
     return y32, blocks
 
 
-def _run_rank(rank, world, port, out):
+def _run_rank(rank, world, port, out, kind):
     import torch.distributed as dist
 
     from paper_1412_4944_b200 import dist as D
@@ -42,7 +45,7 @@ def _run_rank(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         dev = require_device(0)
-        y32, blocks = _problem()
+        y32, blocks = _problem(kind)
         m = y32.shape[0]
         lo, hi = D.shard_range(m, world, rank)
         eng = Engine(Signals.from_rows(y32[lo:hi], dev), 8, k_cap=len(blocks) + 1,
@@ -58,11 +61,12 @@ def _run_rank(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_two_ranks_match_single_process():
+@pytest.mark.parametrize("kind", ["gaussian", "patches"])
+def test_two_ranks_match_single_process(kind):
     from paper_1412_4944_b200.engine import Engine, Signals, require_device
     from paper_1412_4944_b200.sbo import _block_rng
     dev = require_device(0)
-    y32, blocks = _problem()
+    y32, blocks = _problem(kind)
     m = y32.shape[0]
     eng = Engine(Signals.from_rows(y32, dev), 8, k_cap=len(blocks) + 1)
     eng.set_blocks(blocks)
@@ -75,7 +79,7 @@ def test_two_ranks_match_single_process():
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
     port = _free_port()
-    procs = [ctx.Process(target=_run_rank, args=(r, 2, port, out)) for r in range(2)]
+    procs = [ctx.Process(target=_run_rank, args=(r, 2, port, out, kind)) for r in range(2)]
     for pr in procs:
         pr.start()
     for pr in procs:
