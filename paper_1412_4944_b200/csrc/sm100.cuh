@@ -27,13 +27,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// the waiting thread is suspended until the phase completes (or the 10-ms hint
+// expires) instead of re-polling: idle roles stop taking issue slots from the
+// epilogue warps
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "r"(0x989680)
       : "memory");
 }
 
