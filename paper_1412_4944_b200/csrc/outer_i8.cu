@@ -7,14 +7,17 @@
 //   y  = Y_int 2^-Sy, Y_int = sum_a Y_a 128^(4-a), a = 0..4, |Y_a| <= 127
 //        (sign-magnitude digits; exact for float32 signals whose values all sit
 //        on the 2^-Sy grid below 2^(35-Sy) — e.g. unit-range image patches)
-//   x  = X_int 2^-Sx, X_int = sum_b X_b 128^(7-b), b = 0..7, |X_b| <= 64
-//        (balanced digits of the rounded fixed-point code value; |X_int| < 2^54,
-//        resolution 2^-Sx: far below the float64 rounding of P's sums)
+//   x  = X_int 2^-Sx, X_int = sum_b X_b 128^(7-b), b = 0..7: two's-complement
+//        digits of the rounded fixed-point code value (X_0 = X_int >> 49 signed,
+//        X_b = 7-bit fields in [0, 127] below it: 8 independent shift-and-mask
+//        extractions, no carry chain); |X_int| < 2^54, resolution 2^-Sx: far
+//        below the float64 rounding of P's sums)
 //   P[i][j] = 2^(77-Sy-Sx) sum_L D_L[i][j] 128^-L, D_L = sum_{a+b=L} Y_a X_b^T,
 //   levels L <= 7 kept (the dropped levels weigh <= 2^-56 of the product).
 // Every sum is exact integer arithmetic: TMEM int32 per run of consecutive
-// segments of one block (|D_L| <= 5 * 127 * 64 per signal, runs bounded to
-// 2^15 signals), then int64 global accumulators per block (levels 0-3 and 4-7
+// segments of one block (a TMEM column takes <= 4 digit pairs of <= 127 x 127
+// per signal, runs bounded to 2^14 signals: < 2^30), then int64 global
+// accumulators per block (levels 0-3 and 4-7
 // each folded into one int64), so P does not depend on the order of the
 // signals, the segmentation or the grid: bit-identical for any CTA count.
 //
@@ -46,8 +49,8 @@ constexpr int PLANE = P * TS;           // 8 KB
 constexpr int THREADS = 512;
 constexpr int NPROD = THREADS - 128;    // producer threads (warps 4-15)
 constexpr int EPI_DIMS = 8;             // dims per TMEM read batch of the epilogue
-constexpr int64_t RUN_MAX = 1 << 15;    // signals per TMEM accumulation (int32 bound:
-                                        // <= 4 digit pairs x 127 x 64 per signal and region)
+constexpr int64_t RUN_MAX = 1 << 14;    // signals per TMEM accumulation (int32 bound:
+                                        // <= 4 digit pairs x 127 x 127 per signal and region)
 
 constexpr uint32_t YTILE = YD * PLANE;  // one transposed Y digit tile: 40 KB
 
@@ -195,13 +198,12 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
         }
         asm volatile("bar.sync 2, %0;" ::"r"(NPROD));  // X planes zeroed
         auto put = [&](int j, double x, int sl) {
-          long long v = __double2ll_rn(x * xscale);
+          const long long v = __double2ll_rn(x * xscale);
+          const uint32_t off = plane_off(j, sl);
+          xs[xslot(0) * PLANE + off] = static_cast<int8_t>(v >> 49);
 #pragma unroll
-          for (int b = XD - 1; b >= 0; --b) {
-            const int dd = ((static_cast<int>(v) + 64) & 127) - 64;
-            v = (v - dd) >> 7;
-            xs[xslot(b) * PLANE + plane_off(j, sl)] = static_cast<int8_t>(dd);
-          }
+          for (int b = 1; b < XD; ++b)
+            xs[xslot(b) * PLANE + off] = static_cast<int8_t>((v >> (7 * (XD - 1 - b))) & 127);
         };
 #pragma unroll
         for (int c = 0; c < XPRE; ++c)
