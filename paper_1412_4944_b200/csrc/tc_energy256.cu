@@ -505,8 +505,7 @@ extern "C" int sbo_tc_energy256(const void* yhv, const void* ylv, const int16_t*
                : tc256::launch_energy<GG, false>(yh, yl, escale, m, qh, ql, fscale, b0, b1,   \
                                                  k, accumulate, best, score, residual, flags, \
                                                  nflag, cand, st);
-  SBO_TC_CASE(4)
-  SBO_TC_CASE(8)
+  SBO_TC_CASE(8)  // k <= 8 shares the 8-wide network (tc_energy.cu)
   SBO_TC_CASE(16)
   SBO_TC_CASE(32)
 #undef SBO_TC_CASE

@@ -11,3 +11,7 @@ if [ "${FULL_BENCH:-1}" = "1" ]; then
   timeout 900 python bench.py > gpurun_out/bench.log 2>&1
   python -c "import json; d=json.loads(open('gpurun_out/bench.log').read().strip().splitlines()[-1]); print('bench', d['value'], d['ms_per_step'], d['e2e']['value'] if d.get('e2e') else None, d['roofline']['kernel'], d['phases_ms'])"
 fi
+if [ -n "$EXTRA_BENCH" ]; then
+  timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e $EXTRA_BENCH > gpurun_out/bench_extra.log 2>&1
+  python -c "import json; d=json.loads(open('gpurun_out/bench_extra.log').read().strip().splitlines()[-1]); print('extra', d['config']['workload'][:50], d['value'], d['ms_per_step'], {k: round(v['ms_per_step'],2) for k,v in d['kernels'].items()})"
+fi
