@@ -117,7 +117,9 @@ __device__ __forceinline__ uint32_t slab_off(int row, int byte) {
 // integer |v| < 2^51 -> double exactly, without the conversion pipe: the bits
 // of 1.5 2^52 + v, minus 1.5 2^52
 __device__ __forceinline__ double l2d(long long v) {
-  return __longlong_as_double(v + 0x4338000000000000LL) - 6755399441055744.0;
+  // (the magic's low word is 0: only the high word needs the add, no carry)
+  const int hi = static_cast<int>(v >> 32) + 0x43380000;
+  return __hiloint2double(hi, static_cast<int>(v)) - 6755399441055744.0;
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -288,14 +290,19 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
     const int a0 = AQ * part;  // this thread's atoms [a0, a0 + AQ)
     int xb = 0;  // exchange buffer parity
     uint32_t acc_ph = 0;
-    auto bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(EPI_THREADS) : "memory"); };
+    // every exchange is between the NQ warps that hold the same 32 rows (warps
+    // q4, q4 + 4, ...): a named barrier per row group (ids 1-4 sync, 5-8 vote),
+    // so row groups never wait for each other
+    constexpr int GROUP = 32 * NQ;
+    const int bar_id = 1 + q4, vote_id = 5 + q4;
+    auto bar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(GROUP) : "memory"); };
     auto any_of = [&](bool pr) {
       int r;
       asm volatile(
           "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
-          "bar.red.or.pred q, 2, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+          "bar.red.or.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
           : "=r"(r)
-          : "r"(static_cast<int>(pr)), "r"(EPI_THREADS)
+          : "r"(static_cast<int>(pr)), "r"(vote_id), "r"(GROUP)
           : "memory");
       return r != 0;
     };
@@ -470,8 +477,9 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
           }
           bar();
           const int n = static_cast<int>(min64(TS, hi - t0));
-          for (int e = tid; e < k * TS; e += EPI_THREADS) {
-            const int at = e >> 7, rr = e & (TS - 1);
+          // this row group's 32 rows, slot by slot (32 consecutive columns)
+          for (int e = 32 * part + lane; e < k * 32; e += GROUP) {
+            const int at = e >> 5, rr = 32 * q4 + (e & 31);
             if (rr < n) {
               cidx[at * ld + t0 + rr] = S->oidx[at][rr];
               cval[at * ld + t0 + rr] = S->oval[at][rr];
