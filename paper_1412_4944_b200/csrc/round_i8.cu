@@ -74,26 +74,26 @@ struct Roles {
   static constexpr int GMAX = NQ == 2 ? 32 : 16;     // largest top-G list (k <= GMAX)
 };
 
-template <int NQ>
+// shared memory, top-G lists of length G
+template <int NQ, int G>
 struct Smem {
-  static constexpr int GMAX = Roles<NQ>::GMAX;
   int8_t a[2][A_BYTES];
   int8_t b[B_BYTES];
-  int32_t lists[NQ][GMAX][TS];  // [part][rank][row]: per-part top-G keys
+  int32_t lists[NQ][G][TS];     // [part][rank][row]: per-part top-G keys
   int32_t cnt[2][NQ][TS];       // exchange buffers [parity][part][row]
   double part[NQ][2][TS];       // [part][rest | score][row]
-  int16_t oidx[GMAX][TS];       // code outputs staged per (slot, row)
-  double oval[GMAX][TS];
+  int16_t oidx[G][TS];          // code outputs staged per (slot, row)
+  double oval[G][TS];
   uint64_t full[2], empty[2], acc_full, acc_empty, b_full;
   uint32_t tmem;
 };
-template <int NQ>
-constexpr size_t smem_bytes() { return sizeof(Smem<NQ>) + 1024; }
+template <int NQ, int G>
+constexpr size_t smem_bytes() { return sizeof(Smem<NQ, G>) + 1024; }
 
-template <int NQ>
-__device__ __forceinline__ Smem<NQ>* smem_of(unsigned char* raw) {
+template <int NQ, int G>
+__device__ __forceinline__ Smem<NQ, G>* smem_of(unsigned char* raw) {
   const uint32_t a = sm100::smem_u32(raw);
-  return reinterpret_cast<Smem<NQ>*>(raw + ((1024u - (a & 1023u)) & 1023u));
+  return reinterpret_cast<Smem<NQ, G>*>(raw + ((1024u - (a & 1023u)) & 1023u));
 }
 
 __host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
@@ -158,7 +158,8 @@ k_round_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
   constexpr int PROD_WARP0 = R::PROD_WARP0, NPROD = R::NPROD;
   static_assert(G <= R::GMAX, "top-G list longer than the part lists");
   extern __shared__ unsigned char raw[];
-  Smem<NQ>* S = smem_of<NQ>(raw);
+  using SM = Smem<NQ, G>;
+  SM* S = smem_of<NQ, G>(raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nseg = *nseg_p;
   if (tid == 0) {
@@ -557,7 +558,8 @@ static int launch_ri8(unsigned grid, cudaStream_t st, const int8_t* ydig, const 
                       double cscale, int64_t ld, int16_t* idx, double* val, double* rest_sq,
                       double* score) {
   static bool attr = false;
-  constexpr size_t smem = ri8::smem_bytes<NQ>();
+  constexpr size_t smem = ri8::smem_bytes<NQ, G>();
+  static_assert(smem <= 232448, "shared memory over the 227-KB limit");
   if (!attr) {
     SBO_CHECK_CUDA(cudaFuncSetAttribute(ri8::k_round_i8<G, MODE, NQ>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
