@@ -59,9 +59,13 @@ class Comm:
 class TorchComm(Comm):
     """NCCL (or gloo) process group of torch.distributed."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, sharded: bool = False):
+        """``sharded=True`` runs the sharded code path (device-side worst-set select
+        through the collectives) even at world size 1 — how the NCCL capture of the
+        sharded step is tested on a one-GPU box."""
         import torch.distributed as dist
         self.dist, self.group = dist, group
+        self.sharded = sharded
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         # NCCL collectives are stream-ordered device work (CUDA-graph capturable)
@@ -583,7 +587,7 @@ class Engine:
         (members, n, count).  One GPU: n members.  Sharded: at most n members,
         the local count in the device tensor ``count`` (never read back here)."""
         res = self.state.residual
-        if self.comm.world == 1:
+        if self.comm.world == 1 and not getattr(self.comm, "sharded", False):
             n = min(w, self.m)
             members = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
             ws = self.scratch.get("worst", L.size("sbo_worst_workspace_bytes", self.m))
@@ -715,7 +719,8 @@ class Engine:
         repeated iterations from the same entering state on one GPU (the bench):
         replaying it removes the host launch gaps between the ~100 kernels.
         Returns replay() -> IterationOut."""
-        if self.comm.world > 1 and not getattr(self.comm, "capturable", False):
+        if ((self.comm.world > 1 or getattr(self.comm, "sharded", False))
+                and not getattr(self.comm, "capturable", False)):
             raise ValueError("graph capture of a sharded iteration needs NCCL collectives "
                              "(gloo exchanges go through the host)")
         side = torch.cuda.Stream(self.dev)

@@ -94,3 +94,49 @@ def test_two_ranks_match_single_process(kind):
     np.testing.assert_array_equal(np.concatenate([best0, best1]), ref_best)
     np.testing.assert_allclose(np.concatenate([res0, res1]), ref_res, rtol=1e-9, atol=1e-12)
     assert rmse0 == rmse1 and rmse0 == pytest.approx(ref.rmse, rel=1e-12)
+
+
+def test_nccl_sharded_step_captured_as_graph():
+    """The sharded code path on NCCL (one rank: the pool gives one GPU; the
+    collectives still run through NCCL): the worst set's member count stays on
+    the device, so the whole step is captured as one CUDA graph, and replays
+    equal both the eager sharded step and the single-GPU engine."""
+    import torch.distributed as dist
+
+    from paper_1412_4944_b200.engine import Engine, Signals, TorchComm, require_device
+    from paper_1412_4944_b200.sbo import _block_rng
+    dev = require_device(0)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        y32, blocks = _problem("patches")
+        m = y32.shape[0]
+        draws = _block_rng(0, 1, len(blocks)).standard_normal((72, 64))
+        outs = []
+        for comm in (None, TorchComm(sharded=True)):
+            eng = Engine(Signals.from_rows(y32, dev), 8, k_cap=len(blocks) + 1, comm=comm,
+                         m_total=m)
+            eng.set_blocks(blocks)
+            eng.represent_full()
+            snap = eng.snapshot()
+            res = eng.iterate(m // 16, 3, draws)
+            outs.append((eng.blocks[: eng.K].cpu().numpy(), eng.state.best.cpu().numpy(),
+                         res.rmse, np.sort(res.worst.cpu().numpy())))
+            if comm is not None:
+                assert comm.capturable
+                replay = eng.capture_iteration(snap, m // 16, 3,
+                                               torch.from_numpy(draws).to(dev))
+                for _ in range(2):
+                    r2 = replay()
+                    outs.append((eng.blocks[: eng.K].cpu().numpy(),
+                                 eng.state.best.cpu().numpy(), r2.rmse,
+                                 np.sort(r2.worst.cpu().numpy())))
+        ref = outs[0]
+        for b, best, rmse, worst in outs[1:]:
+            np.testing.assert_array_equal(best, ref[1])
+            np.testing.assert_array_equal(worst, ref[3])
+            assert np.abs(b - ref[0]).max() < 1e-12
+            assert rmse == pytest.approx(ref[2], rel=1e-13)
+    finally:
+        dist.destroy_process_group()

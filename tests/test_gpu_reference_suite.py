@@ -193,6 +193,21 @@ def test_block_energy_cases():  # test_sbo.py:42-68
         S.block_energy(np.ones(2), np.eye(2), 1, "other")
 
 
+@pytest.mark.parametrize("p,s0", [(64, 8), (64, 3), (256, 16)])
+def test_block_energy_tensor_core_shapes_exact(p, s0):
+    """p = 64 / 256 (the shapes whose representation runs on the tensor cores):
+    block_energy is the exact float64 value (oracle energy_of, sbo.py:126-135)
+    for both kinds, not the float32 certificate score."""
+    from oracle import sbo_oracle as O
+    rng = np.random.default_rng(p + s0)
+    q = orth(p, rng)
+    for _ in range(4):
+        y = rng.standard_normal(p)
+        for kind in ("squared-sum", "abs-sum"):
+            ref = O.energy_of(y, q, s0, kind)
+            assert S.block_energy(y, q, s0, kind) == pytest.approx(ref, rel=1e-12)
+
+
 # ----------------------------------------------------------------- represent
 def test_represent_contracts():  # test_sbo.py:71-165
     rng = np.random.default_rng(70)
