@@ -583,7 +583,10 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
     else:
         host_in = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in ingest]
     host_blocks = snap_blocks[:K0].cpu().pin_memory()
-    host_state = [t.cpu().pin_memory() for t in snap]
+    # the entering state the iteration reads: best, score, residual, total (the
+    # signal norms, snap[2], are not read by it and stay on the device)
+    up_idx = (0, 1, 3, 4)
+    host_state = [snap[i].cpu().pin_memory() for i in up_idx]
     host_draws = torch.from_numpy(np.ascontiguousarray(draws, dtype=np.float64)).pin_memory()
     out_blocks = torch.empty((K0 + 1,) + tuple(snap_blocks.shape[1:]), dtype=torch.float64).pin_memory()
     out_best = torch.empty(rows.shape[0], dtype=torch.int32).pin_memory()
@@ -619,8 +622,8 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
             if freed[j] is not None:
                 copier.wait_event(freed[j])
             stg[j]["blocks"][:K0].copy_(host_blocks, non_blocking=True)
-            for dst, src in zip(stg[j]["state"], host_state):
-                dst.copy_(src, non_blocking=True)
+            for i, src in zip(up_idx, host_state):
+                stg[j]["state"][i].copy_(src, non_blocking=True)
             dev_draws[j].copy_(host_draws, non_blocking=True)
             for dst, src in zip(dev_in[j], host_in):
                 dst.copy_(src, non_blocking=True)
@@ -640,8 +643,8 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
     if dist is None and os.environ.get("SBO_BENCH_NO_GRAPH", "0") != "1":
         for j in range(2):
             stg[j]["blocks"][:K0].copy_(host_blocks.to(eng.dev))
-            for dst, src in zip(stg[j]["state"], host_state):
-                dst.copy_(src.to(eng.dev))
+            for i, src in zip(up_idx, host_state):
+                stg[j]["state"][i].copy_(src.to(eng.dev))
             dev_draws[j].copy_(host_draws.to(eng.dev))
             for dst, src in zip(dev_in[j], host_in):
                 dst.copy_(src.to(eng.dev))
