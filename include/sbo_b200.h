@@ -101,31 +101,32 @@ int sbo_tc_split_blocks(const double* Q, int K, int p, void* qh, void* ql, int16
 int sbo_tc_energy(const void* yh, const void* yl, const int16_t* escale, int64_t m,
                   const void* qh, const void* ql, const int16_t* fscale, int b0, int b1, int s0,
                   int kind, int accumulate, int32_t* best, double* score, double* residual_sq,
-                  int32_t* flags, int32_t* nflag, int32_t* cand, void* stream);
+                  int32_t* flags, int32_t* nflag, uint64_t* cand, void* stream);
 /* p = 256 (config D), s0 <= 32: the same contract as sbo_tc_energy on operands
  * from sbo_tc_split_signals / sbo_tc_split_blocks with p = 256 (tc_energy256.cu). */
 int sbo_tc_energy256(const void* yh, const void* yl, const int16_t* escale, int64_t m,
                      const void* qh, const void* ql, const int16_t* fscale, int b0, int b1,
                      int s0, int kind, int accumulate, int32_t* best, double* score,
-                     double* residual, int32_t* flags, int32_t* nflag, int32_t* cand,
+                     double* residual, int32_t* flags, int32_t* nflag, uint64_t* cand,
                      void* stream);
 
 /* Candidate blocks of the flagged signals (cand, optional, parallel to flags):
  * bit b - b0 set for every block whose approximate decision value was within
- * the certificate's tolerance of the best (all bits when b1 - b0 > 32) — a
+ * the certificate's tolerance of the best (b1 - b0 <= 64; the p = 256 pass sets
+ * every bit above 32 blocks) — a
  * superset of the blocks that can win in float64.  sbo_cand_sort orders the
  * flag list by its two lowest candidate blocks, so that tiles of the float64
  * re-decision share few blocks (order within a group is arbitrary: each
  * signal's decision is independent of it).  Workspace: sbo_cand_workspace_bytes. */
 size_t sbo_cand_workspace_bytes(void);
-int sbo_cand_sort(const int32_t* flags, const int32_t* cand, const int32_t* nflag,
-                  int64_t max_list, int32_t* flags_out, int32_t* cand_out, void* ws,
+int sbo_cand_sort(const int32_t* flags, const uint64_t* cand, const int32_t* nflag,
+                  int64_t max_list, int32_t* flags_out, uint64_t* cand_out, void* ws,
                   size_t ws_bytes, void* stream);
 
 /* sbo_energy_recheck restricted per tile to the union of the listed signals'
- * candidate blocks (cand parallel to list; blocks b0 + bit), b1 - b0 <= 32. */
+ * candidate blocks (cand parallel to list; blocks b0 + bit), b1 - b0 <= 64. */
 int sbo_energy_recheck_cand(const void* y, int dtype, int64_t m, int p, const double* blocks,
-                            int K, int s0, int kind, const int32_t* list, const int32_t* cand,
+                            int K, int s0, int kind, const int32_t* list, const uint64_t* cand,
                             const int32_t* nlist, int64_t max_list, int32_t* best, double* score,
                             double* residual_sq, void* stream);
 

@@ -587,22 +587,22 @@ extern "C" int sbo_worst_collect(const double* residual_sq, int64_t m, uint64_t 
 // ---------------------------------------------------------------------------
 // ordering of the flagged signals by their two lowest candidate blocks
 // ---------------------------------------------------------------------------
-constexpr int kCandKeys = 32 * 33;
+constexpr int kCandKeys = 64 * 65;
 
-__device__ __forceinline__ int cand_key(uint32_t mask) {
-  const int lo = mask ? __ffs(static_cast<int>(mask)) - 1 : 0;
-  const uint32_t rest = mask & (mask - 1u);
-  const int hi = rest ? __ffs(static_cast<int>(rest)) - 1 : 32;
-  return lo * 33 + hi;
+__device__ __forceinline__ int cand_key(uint64_t mask) {
+  const int lo = mask ? __ffsll(static_cast<long long>(mask)) - 1 : 0;
+  const uint64_t rest = mask & (mask - 1ull);
+  const int hi = rest ? __ffsll(static_cast<long long>(rest)) - 1 : 64;
+  return lo * 65 + hi;
 }
 
-__global__ void k_cand_hist(const int32_t* __restrict__ cand, const int32_t* nflag, int* cnt) {
+__global__ void k_cand_hist(const uint64_t* __restrict__ cand, const int32_t* nflag, int* cnt) {
   __shared__ int h[kCandKeys];
   for (int i = threadIdx.x; i < kCandKeys; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const int n = *nflag;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAdd(&h[cand_key(static_cast<uint32_t>(cand[i]))], 1);
+    atomicAdd(&h[cand_key(cand[i])], 1);
   __syncthreads();
   for (int i = threadIdx.x; i < kCandKeys; i += blockDim.x)
     if (h[i]) atomicAdd(&cnt[i], h[i]);
@@ -611,7 +611,7 @@ __global__ void k_cand_hist(const int32_t* __restrict__ cand, const int32_t* nfl
 __global__ void __launch_bounds__(1024) k_cand_scan(int* cnt) {
   __shared__ int wsum[32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  constexpr int PER = (kCandKeys + 1023) / 1024;  // keys per thread (2)
+  constexpr int PER = (kCandKeys + 1023) / 1024;  // keys per thread (5)
   int v[PER], tot = 0;
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
@@ -646,22 +646,22 @@ __global__ void __launch_bounds__(1024) k_cand_scan(int* cnt) {
   }
 }
 
-__global__ void k_cand_scatter(const int32_t* __restrict__ flags, const int32_t* __restrict__ cand,
+__global__ void k_cand_scatter(const int32_t* __restrict__ flags, const uint64_t* __restrict__ cand,
                                const int32_t* nflag, int* off, int32_t* flags_out,
-                               int32_t* cand_out) {
+                               uint64_t* cand_out) {
   const int n = *nflag;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t mk = static_cast<uint32_t>(cand[i]);
+    const uint64_t mk = cand[i];
     const int at = atomicAdd(&off[cand_key(mk)], 1);
     flags_out[at] = flags[i];
-    cand_out[at] = static_cast<int32_t>(mk);
+    cand_out[at] = mk;
   }
 }
 
 extern "C" size_t sbo_cand_workspace_bytes(void) { return sizeof(int) * kCandKeys + 64; }
 
-extern "C" int sbo_cand_sort(const int32_t* flags, const int32_t* cand, const int32_t* nflag,
-                             int64_t max_list, int32_t* flags_out, int32_t* cand_out, void* ws,
+extern "C" int sbo_cand_sort(const int32_t* flags, const uint64_t* cand, const int32_t* nflag,
+                             int64_t max_list, int32_t* flags_out, uint64_t* cand_out, void* ws,
                              size_t ws_bytes, void* stream) {
   if (ws_bytes < sbo_cand_workspace_bytes()) return fail(SBO_EINVAL, "cand workspace too small");
   if (!flags || !cand || !nflag || !flags_out || !cand_out) return fail(SBO_EINVAL, "null list");

@@ -42,7 +42,9 @@ struct Smem {
   uint32_t tmem;
   float x_r1[M], x_r2[M], x_s[M], x_rb[M], x_eb[M];
   int x_b1[M];
-  float x_dec[32][M];  // decision value per (block - b0, signal) for the candidate masks
+  // decision value per (block - b0, signal) for the candidate masks, in fp16
+  // (compared with a 2^-10 relative margin: the masks stay supersets)
+  __half x_dec[64][M];
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 
@@ -75,9 +77,10 @@ __device__ __forceinline__ float resid_err(float r, float s, float d, int n) {
 }
 
 // candidate mask of a signal flagged by an incremental pass over [b0, b1)
-// (b1 <= 32): its incoming winner and every appended block
-__device__ __forceinline__ uint32_t accum_cand(int prev, int b0, int b1) {
-  return (prev >= 0 && prev < 32 ? 1u << prev : 0u) | (((1u << (b1 - b0)) - 1u) << b0);
+// (b1 <= 64): its incoming winner and every appended block
+__device__ __forceinline__ uint64_t accum_cand(int prev, int b0, int b1) {
+  const uint64_t app = (b1 - b0 >= 64 ? ~0ull : ((1ull << (b1 - b0)) - 1ull)) << b0;
+  return (prev >= 0 && prev < 64 ? 1ull << prev : 0ull) | app;
 }
 
 template <int G, bool ABS>
@@ -86,7 +89,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
             const int16_t* __restrict__ escale, int64_t m, const __half* __restrict__ qh,
             const __half* __restrict__ ql, const int16_t* __restrict__ fscale, int b0, int b1,
             int ksel, int accumulate, int32_t* best, double* score, double* residual,
-            int32_t* flags, int32_t* nflag, int32_t* cand) {
+            int32_t* flags, int32_t* nflag, uint64_t* cand) {
   extern __shared__ unsigned char raw[];
   Smem* S = smem_of(raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -271,7 +274,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           if (flag) {
             const int ix = atomicAdd(nflag, 1);
             flags[ix] = static_cast<int32_t>(j);
-            if (cand) cand[ix] = static_cast<int32_t>(accum_cand(__ldcg(best + j), b0, b1));
+            if (cand) cand[ix] = accum_cand(__ldcg(best + j), b0, b1);
           }
         } else {
           best[j] = b0;
@@ -314,7 +317,7 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
             d2 = dec;
           }
           snorm = sq;
-          if (cand && b - b0 < 32) S->x_dec[b - b0][row] = dec;
+          if (cand && b - b0 < 64) S->x_dec[b - b0][row] = __float2half_ru(dec);
         }
         sm100::tc_fence_before();
         __syncwarp();
@@ -373,20 +376,21 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
           if (cand && accumulate) {
             // incremental pass: the incoming winner and the appended blocks, all
             // re-evaluated by the same float64 kernel (exact ties -> lower block)
-            cand[ix] = static_cast<int32_t>(accum_cand(__ldcg(best + j), b0, b1));
+            cand[ix] = accum_cand(__ldcg(best + j), b0, b1);
           } else if (cand) {
             // candidate blocks: within the certificate's tolerance of the final best
-            // (1 % slack on the bound); all blocks when more than 32
-            uint32_t cmask = 0xFFFFFFFFu;
-            if (nblk <= 32) {
-              cmask = 0u;
-              const float lim = d1 + 1.01f * err(d1);
-              for (int jb = 0; jb < nblk; ++jb) {
-                const float dv = S->x_dec[jb][row];
-                if (dv <= lim + 1.01f * err(dv)) cmask |= 1u << jb;
-              }
+            // (1 % slack on the bound; the fp16 decision values were rounded up,
+            // and 2^-10 of |dv| more covers a downward rounding of dv)
+            uint64_t cmask = 0ull;
+            const float lim = d1 + 1.01f * err(d1);
+            for (int jb = 0; jb < nblk; ++jb) {
+              const float h = __half2float(S->x_dec[jb][row]);
+              // fp16 spacing: 2^-10 relative, 2^-24 absolute near zero; an
+              // out-of-range value (inf) is always a candidate
+              const float slack = fabsf(h) * 9.765625e-4f + 6.0e-8f;
+              if (!isfinite(h) || h - slack <= lim + 1.01f * err(h) + slack) cmask |= 1ull << jb;
             }
-            cand[ix] = static_cast<int32_t>(cmask);
+            cand[ix] = cmask;
           }
         }
       }
@@ -473,7 +477,7 @@ template <int G, bool ABS>
 int launch_energy(const __half* yh, const __half* yl, const int16_t* es, int64_t m,
                   const __half* qh, const __half* ql, const int16_t* fs, int b0, int b1, int ksel,
                   int accumulate, int32_t* best, double* score, double* residual,
-                  int32_t* flags, int32_t* nflag, int32_t* cand, cudaStream_t st) {
+                  int32_t* flags, int32_t* nflag, uint64_t* cand, cudaStream_t st) {
   auto kern = k_energy_tc<G, ABS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(SMEM_BYTES));
@@ -529,7 +533,7 @@ extern "C" int sbo_tc_energy(const void* yhv, const void* ylv, const int16_t* es
                              int64_t m, const void* qhv, const void* qlv,
                              const int16_t* fscale, int b0, int b1, int s0, int kind,
                              int accumulate, int32_t* best, double* score, double* residual,
-                             int32_t* flags, int32_t* nflag, int32_t* cand, void* stream) {
+                             int32_t* flags, int32_t* nflag, uint64_t* cand, void* stream) {
   const __half* yh = static_cast<const __half*>(yhv);
   const __half* yl = static_cast<const __half*>(ylv);
   const __half* qh = static_cast<const __half*>(qhv);
@@ -537,6 +541,7 @@ extern "C" int sbo_tc_energy(const void* yhv, const void* ylv, const int16_t* es
   if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
   if (b0 < 0 || b1 <= b0 || (!accumulate && b0 != 0))
     return fail(SBO_EINVAL, "bad block range for the energy pass");
+  if (cand && b1 > 64) return fail(SBO_EINVAL, "candidate masks cover at most 64 blocks");
   if (m == 0) return SBO_OK;
   const int k = s0 < tc::P ? s0 : tc::P;
   cudaStream_t st = as_stream(stream);

@@ -77,8 +77,9 @@ __device__ __forceinline__ float resid_err(float r, float d, int n) {
 
 // candidate mask of a signal flagged by an incremental pass over [b0, b1)
 // (b1 <= 32): its incoming winner and every appended block
-__device__ __forceinline__ uint32_t accum_cand(int prev, int b0, int b1) {
-  return (prev >= 0 && prev < 32 ? 1u << prev : 0u) | (((1u << (b1 - b0)) - 1u) << b0);
+__device__ __forceinline__ uint64_t accum_cand(int prev, int b0, int b1) {
+  const uint64_t app = (b1 - b0 >= 64 ? ~0ull : ((1ull << (b1 - b0)) - 1ull)) << b0;
+  return (prev >= 0 && prev < 64 ? 1ull << prev : 0ull) | app;
 }
 
 template <int G, bool ABS>
@@ -87,7 +88,7 @@ k_energy_tc256(const __half* __restrict__ yh, const __half* __restrict__ yl,
                const int16_t* __restrict__ escale, int64_t m, const __half* __restrict__ qh,
                const __half* __restrict__ ql, const int16_t* __restrict__ fscale, int b0, int b1,
                int ksel, int accumulate, int32_t* best, double* score, double* residual,
-               int32_t* flags, int32_t* nflag, int32_t* cand) {
+               int32_t* flags, int32_t* nflag, uint64_t* cand) {
   extern __shared__ unsigned char raw[];
   Smem* S = smem_of(raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -330,20 +331,20 @@ k_energy_tc256(const __half* __restrict__ yh, const __half* __restrict__ yl,
           if (cand && accumulate) {
             // incremental pass: the incoming winner and the appended blocks, all
             // re-evaluated by the same float64 kernel (exact ties -> lower block)
-            cand[ix] = static_cast<int32_t>(accum_cand(__ldcg(best + j), b0, b1));
+            cand[ix] = accum_cand(__ldcg(best + j), b0, b1);
           } else if (cand) {
             // candidate blocks: within the certificate's tolerance of the final best
             // (1 % slack on the bound); all blocks when more than 32
-            uint32_t cmask = 0xFFFFFFFFu;
+            uint64_t cmask = ~0ull;
             if (nblk <= 32) {
-              cmask = 0u;
+              cmask = 0ull;
               const float lim = d1 + 1.01f * err(d1);
               for (int jb = 0; jb < nblk; ++jb) {
                 const float dv = S->x_dec[jb][row];
-                if (dv <= lim + 1.01f * err(dv)) cmask |= 1u << jb;
+                if (dv <= lim + 1.01f * err(dv)) cmask |= 1ull << jb;
               }
             }
-            cand[ix] = static_cast<int32_t>(cmask);
+            cand[ix] = cmask;
           }
         }
       }
@@ -439,7 +440,7 @@ template <int G, bool ABS>
 int launch_energy(const __half* yh, const __half* yl, const int16_t* es, int64_t m,
                   const __half* qh, const __half* ql, const int16_t* fs, int b0, int b1, int ksel,
                   int accumulate, int32_t* best, double* score, double* residual,
-                  int32_t* flags, int32_t* nflag, int32_t* cand, cudaStream_t st) {
+                  int32_t* flags, int32_t* nflag, uint64_t* cand, cudaStream_t st) {
   auto kern = k_energy_tc256<G, ABS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(SMEM_BYTES));
@@ -485,7 +486,7 @@ extern "C" int sbo_tc_energy256(const void* yhv, const void* ylv, const int16_t*
                                 int64_t m, const void* qhv, const void* qlv,
                                 const int16_t* fscale, int b0, int b1, int s0, int kind,
                                 int accumulate, int32_t* best, double* score, double* residual,
-                                int32_t* flags, int32_t* nflag, int32_t* cand, void* stream) {
+                                int32_t* flags, int32_t* nflag, uint64_t* cand, void* stream) {
   const __half* yh = static_cast<const __half*>(yhv);
   const __half* yl = static_cast<const __half*>(ylv);
   const __half* qh = static_cast<const __half*>(qhv);
@@ -493,6 +494,7 @@ extern "C" int sbo_tc_energy256(const void* yhv, const void* ylv, const int16_t*
   if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
   if (b0 < 0 || b1 <= b0 || (!accumulate && b0 != 0))
     return fail(SBO_EINVAL, "bad block range for the energy pass");
+  if (cand && b1 > 64) return fail(SBO_EINVAL, "candidate masks cover at most 64 blocks");
   if (m == 0) return SBO_OK;
   const int k = s0 < tc256::P ? s0 : tc256::P;
   cudaStream_t st = as_stream(stream);

@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
     const TY* __restrict__ y, int64_t m, int p, const double* __restrict__ blocks, int b0,
     int b1, int k, int kind, int accumulate, const int32_t* __restrict__ list,
     const int32_t* __restrict__ nlist, int32_t* best, double* score, double* rest_sq,
-    double* norm_sq, const int32_t* __restrict__ cand) {
+    double* norm_sq, const uint64_t* __restrict__ cand) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned tile_cand;  // union of the tile's candidate blocks (bit b - b0)
+  __shared__ unsigned long long tile_cand;  // union of the tile's candidate blocks (bit b - b0)
   const TileLayout L(p);
   double* C = reinterpret_cast<double*>(smem + L.c_off);
   double* sY = reinterpret_cast<double*>(smem + L.y_off);
@@ -253,16 +253,16 @@ __global__ void __launch_bounds__(kThreads) k_energy_f64(
         brest[threadIdx.x] = 0.0;
       }
     }
-    if (threadIdx.x == 0) tile_cand = cand ? 0u : 0xFFFFFFFFu;
+    if (threadIdx.x == 0) tile_cand = cand ? 0ull : ~0ull;
     __syncthreads();
     if (cand && threadIdx.x < kTile && base + threadIdx.x < count)
-      atomicOr(&tile_cand, static_cast<unsigned>(cand[base + threadIdx.x]));
+      atomicOr(&tile_cand, static_cast<unsigned long long>(cand[base + threadIdx.x]));
     __syncthreads();
-    const unsigned tcand = tile_cand;
+    const unsigned long long tcand = tile_cand;
     int* fb = bbest + kTile;  // per-signal "needs the exact rank method" marks
     if (p <= 64) stage_y64(y, p, rows, sY);
     for (int b = b0; b < b1; ++b) {
-      if (b - b0 < 32 && !((tcand >> (b - b0)) & 1u)) continue;  // no signal of the tile can win here
+      if (b - b0 < 64 && !((tcand >> (b - b0)) & 1ull)) continue;  // no signal of the tile can win here
       if (p <= 64) {
         __syncthreads();
         stage_q64(blocks + static_cast<int64_t>(b) * p * p, p, sQ);
@@ -614,7 +614,7 @@ template <typename TY>
 int energy_impl(const void* yv, int64_t m, int p, const double* blocks, int b0, int b1, int k,
                 int kind, int accumulate, const int32_t* list, const int32_t* nlist,
                 int64_t max_list, int32_t* best, double* score, double* rest_sq,
-                double* norm_sq, cudaStream_t st, const int32_t* cand = nullptr) {
+                double* norm_sq, cudaStream_t st, const uint64_t* cand = nullptr) {
   const TileLayout L(p);
   cudaFuncSetAttribute(k_energy_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
@@ -700,12 +700,12 @@ extern "C" int sbo_energy_recheck(const void* y, int dtype, int64_t m, int p,
 
 extern "C" int sbo_energy_recheck_cand(const void* y, int dtype, int64_t m, int p,
                                        const double* blocks, int K, int s0, int kind,
-                                       const int32_t* list, const int32_t* cand,
+                                       const int32_t* list, const uint64_t* cand,
                                        const int32_t* nlist, int64_t max_list, int32_t* best,
                                        double* score, double* residual_sq, void* stream) {
   if (int rc = check_common(dtype, p, s0)) return rc;
-  if (K < 1 || K > 32 || !list || !cand || !nlist)
-    return fail(SBO_EINVAL, "candidate recheck needs 1 <= K <= 32, a list and its masks");
+  if (K < 1 || K > 64 || !list || !cand || !nlist)
+    return fail(SBO_EINVAL, "candidate recheck needs 1 <= K <= 64, a list and its masks");
   if (max_list <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
   return dtype == SBO_F32

@@ -367,19 +367,20 @@ class Engine:
                        self.ql.data_ptr() + 2 * b0 * pp, self.fscale.data_ptr() + 2 * b0,
                        self.stream)
             self.nflag.zero_()
-            # <= 32 blocks: the flagged signals carry candidate-block masks (full
+            # <= 64 blocks: the flagged signals carry candidate-block masks (full
             # pass: the blocks within the certificate's tolerance of the best;
             # incremental pass: the incoming winner and the appended blocks);
             # sorted by them, the float64 tiles only visit their union.  Every
             # candidate is re-evaluated by the same float64 kernel, so exact ties
             # go to the lower block (sbo.py:191) whatever kernel produced the
             # stored scores.
-            use_cand = b1 <= 32
+            use_cand = b1 <= 64
             if use_cand and getattr(self, "cand", None) is None:
                 i32 = dict(dtype=torch.int32, device=self.dev)
-                self.cand = torch.empty(self.m, **i32)
+                i64 = dict(dtype=torch.int64, device=self.dev)
+                self.cand = torch.empty(self.m, **i64)          # 64-bit block masks
                 self.flags_sorted = torch.empty(self.m, **i32)
-                self.cand_sorted = torch.empty(self.m, **i32)
+                self.cand_sorted = torch.empty(self.m, **i64)
             self._call("sbo_tc_energy" if self.p == 64 else "sbo_tc_energy256",
                        self.yh.data_ptr(), self.yl.data_ptr(),
                        self.escale.data_ptr(), self.m, self.qh.data_ptr(), self.ql.data_ptr(),
@@ -399,7 +400,7 @@ class Engine:
                            self.nflag.data_ptr(), self.m, s.best.data_ptr(),
                            s.score.data_ptr(), s.residual.data_ptr(), self.stream)
             else:
-                # more than 32 blocks: the flagged signals are re-decided over every
+                # more than 64 blocks: the flagged signals are re-decided over every
                 # block from scratch
                 self._call("sbo_energy_recheck", self.sig.y.data_ptr(), self.sig.code, self.m,
                            self.p, self.blocks.data_ptr(), 0, b1,
