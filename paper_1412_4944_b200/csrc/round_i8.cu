@@ -544,7 +544,10 @@ __global__ void k_q_digits(const double* __restrict__ blocks, int b0, int nb,
 using namespace sbo;
 
 #ifndef RI8_NQ
-#define RI8_NQ 2  // epilogue atom parts for s0 <= 16 (4 parts, 16 epilogue warps: measured slower, 25.5 vs 22.8 ms per config-C iteration)
+#define RI8_NQ 2  // epilogue atom parts of the code mode for s0 <= 16
+#endif
+#ifndef RI8_NQ_RESID
+#define RI8_NQ_RESID 4  // epilogue atom parts of the residual mode for s0 <= 16
 #endif
 
 extern "C" size_t sbo_round_i8_workspace_bytes(int nblocks) {
@@ -602,16 +605,22 @@ extern "C" int sbo_round_i8_segments(const void* ydig, int sy, const int32_t* or
   const unsigned grid = static_cast<unsigned>(min64(max_seg, sms));
   const double cscale = ldexp(1.0, -sy - 26);
   const auto* yd = static_cast<const int8_t*>(ydig);
-#define RI8_GO(G_, NQ_)                                                                       \
+// code mode: 2 atom parts (8 epilogue warps); residual mode (no staged code
+// outputs): 4 parts (16 epilogue warps) for s0 <= 16 — measured per mode
+// (A/B per iteration: code 29.2 vs 37.0 ms of retrain with 2 vs 4 parts,
+// residual 20.4 vs 21.6 ms of represent #2 with 4 vs 2)
+#define RI8_GO(G_, NQC_, NQR_)                                                                \
   return mode == ri8::MODE_CODE                                                                \
-             ? launch_ri8<G_, ri8::MODE_CODE, NQ_>(grid, st, yd, order, seg_block, seg_lo, seg_hi,  \
-                                              nseg, qdig, block_override, s0, kind, cscale,     \
-                                              ld, idx, val, rest_sq, score)               \
-             : launch_ri8<G_, ri8::MODE_RESID, NQ_>(grid, st, yd, order, seg_block, seg_lo, seg_hi, \
-                                               nseg, qdig, block_override, s0, kind, cscale,    \
-                                               ld, idx, val, rest_sq, score)
-  if (s0 <= 8) RI8_GO(8, RI8_NQ);
-  if (s0 <= 16) RI8_GO(16, RI8_NQ);
-  RI8_GO(32, 2);
+             ? launch_ri8<G_, ri8::MODE_CODE, NQC_>(grid, st, yd, order, seg_block, seg_lo,    \
+                                                    seg_hi, nseg, qdig, block_override, s0,    \
+                                                    kind, cscale, ld, idx, val, rest_sq,       \
+                                                    score)                                     \
+             : launch_ri8<G_, ri8::MODE_RESID, NQR_>(grid, st, yd, order, seg_block, seg_lo,   \
+                                                     seg_hi, nseg, qdig, block_override, s0,   \
+                                                     kind, cscale, ld, idx, val, rest_sq,      \
+                                                     score)
+  if (s0 <= 8) RI8_GO(8, RI8_NQ, RI8_NQ_RESID);
+  if (s0 <= 16) RI8_GO(16, RI8_NQ, RI8_NQ_RESID);
+  RI8_GO(32, 2, 2);
 #undef RI8_GO
 }
