@@ -635,7 +635,7 @@ def run_e2e(a, eng, rows, snap_blocks, snap, K0, w, draws, dist, ingest=None):
             g, r, c = dev_in[j]
             D.extract_rows(g, D.GRID_U8, a.p_edge, r, c, "unit-range", out=ybuf[j],
                            stream=eng.stream)
-        eng.refresh_signals(rescan=False)  # device-side operand split (same digit format)
+        eng.refresh_signals(rescan=False)  # operand split + digit rows of the new signals
         return eng.iterate_device(w, a.rounds, dev_draws[j])
 
     # one GPU: each set's step (restore + operand split + iteration) as a CUDA graph

@@ -237,16 +237,21 @@ class Engine:
         self.refresh_signals()
 
     def refresh_signals(self, rescan: bool = True):
-        """Re-derive the tensor-core operands (split fp16) after the signals changed;
-        ``rescan`` re-checks the integer-digit format of the training rounds (a
-        host synchronisation: pass False when the new signals are known to share
-        the old ones' format, e.g. inside a captured CUDA graph)."""
+        """Re-derive every device operand of the signals after they changed: the
+        tensor-core split (fp16 hi/lo) and the integer digits of the training
+        rounds.  ``rescan`` also re-checks the digit format (a host
+        synchronisation); pass False when the new signals are known to share the
+        old ones' format (e.g. inside a captured CUDA graph): the digit rows are
+        then rebuilt in the existing format."""
         if self.tc:
             self._call("sbo_tc_split_signals", self.sig.y.data_ptr(), self.sig.code, self.m,
                        self.p, self.yh.data_ptr(), self.yl.data_ptr(), self.escale.data_ptr(),
                        self.stream)
         if rescan:
             self._scan_digits()
+        elif self.i8 is not None:
+            self._call("sbo_y_digits", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
+                       self.i8[0], self.ydig.data_ptr(), self.stream)
 
     def _scan_digits(self):
         """Digit formats of the tensor-core outer product (outer_i8.cu): p = 64,
