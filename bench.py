@@ -97,15 +97,22 @@ def shard_signals(a, rank, world):
     return signals.unit_range(u8), a.m_total
 
 
+def relaunch_args(gpus: int, port: int, argv: list[str]) -> list[str]:
+    """torch.distributed.run arguments that re-run this script with `argv` on
+    `gpus` ranks (tests/test_bench_cli.py: every bench option survives the
+    launcher's own parser)."""
+    return ["--nnodes=1", f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+            f"--master-port={port}", str(Path(__file__).resolve())] + list(argv)
+
+
 def relaunch_distributed(a):
     """--gpus N > 1 outside torchrun: run this script under torch.distributed.run."""
     import socket
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
-           str(Path(__file__).resolve())] + sys.argv[1:]
+    cmd = [sys.executable, "-m", "torch.distributed.run"] + relaunch_args(a.gpus, port,
+                                                                          sys.argv[1:])
     sys.exit(subprocess.call(cmd))
 
 
