@@ -42,9 +42,13 @@ struct Smem {
   uint32_t tmem;
   float x_r1[M], x_r2[M], x_s[M], x_rb[M], x_eb[M];
   int x_b1[M];
-  // decision value per (block - b0, signal) for the candidate masks, in fp16
-  // (compared with a 2^-10 relative margin: the masks stay supersets)
-  __half x_dec[64][M];
+  // decision value per (block - b0, signal) for the candidate masks: fp32 up to
+  // 32 blocks, fp16 up to 64 (compared with a 2^-10 relative margin, so the masks
+  // stay supersets; wider than the fp32 ones, hence only above 32 blocks)
+  union {
+    float f[32][M];
+    __half h[64][M];
+  } x_dec;
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 
@@ -317,7 +321,10 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
             d2 = dec;
           }
           snorm = sq;
-          if (cand && b - b0 < 64) S->x_dec[b - b0][row] = __float2half_ru(dec);
+          if (cand) {
+            if (nblk <= 32) S->x_dec.f[b - b0][row] = dec;
+            else if (b - b0 < 64) S->x_dec.h[b - b0][row] = __float2half_ru(dec);
+          }
         }
         sm100::tc_fence_before();
         __syncwarp();
@@ -383,12 +390,19 @@ k_energy_tc(const __half* __restrict__ yh, const __half* __restrict__ yl,
             // and 2^-10 of |dv| more covers a downward rounding of dv)
             uint64_t cmask = 0ull;
             const float lim = d1 + 1.01f * err(d1);
-            for (int jb = 0; jb < nblk; ++jb) {
-              const float h = __half2float(S->x_dec[jb][row]);
-              // fp16 spacing: 2^-10 relative, 2^-24 absolute near zero; an
-              // out-of-range value (inf) is always a candidate
-              const float slack = fabsf(h) * 9.765625e-4f + 6.0e-8f;
-              if (!isfinite(h) || h - slack <= lim + 1.01f * err(h) + slack) cmask |= 1ull << jb;
+            if (nblk <= 32) {
+              for (int jb = 0; jb < nblk; ++jb) {
+                const float dv = S->x_dec.f[jb][row];
+                if (dv <= lim + 1.01f * err(dv)) cmask |= 1ull << jb;
+              }
+            } else {
+              for (int jb = 0; jb < nblk; ++jb) {
+                const float h = __half2float(S->x_dec.h[jb][row]);
+                // fp16 spacing: 2^-10 relative, 2^-24 absolute near zero; an
+                // out-of-range value (inf) is always a candidate
+                const float slack = fabsf(h) * 9.765625e-4f + 6.0e-8f;
+                if (!isfinite(h) || h - slack <= lim + 1.01f * err(h) + slack) cmask |= 1ull << jb;
+              }
             }
             cand[ix] = cmask;
           }
