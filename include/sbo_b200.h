@@ -249,8 +249,9 @@ int sbo_y_tiles(const void* ydig, const int32_t* order, const int64_t* seg_lo,
                 const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg, void* tiles,
                 void* stream);
 
-/* Signal-major digit rows of float32 signals for sbo_outer_i8_segments: row s
- * (320 bytes) = the 5 digit planes Y_a (64 dims each) of y_s = Y_int 2^-sy. */
+/* Signal-major digit rows of float32 signals (p = 64 or 256) for
+ * sbo_outer_i8_segments / sbo_round_i8_segments / sbo_coef_i8_segments: row s
+ * (5 p bytes) = the 5 digit planes Y_a (p dims each) of y_s = Y_int 2^-sy. */
 int sbo_y_digits(const void* y, int dtype, int64_t m, int p, int sy, void* ydig, void* stream);
 
 /* Digit-format scan of float32 signals (m rows of p): out[0] = smallest E with
@@ -292,6 +293,33 @@ int sbo_chunk_segments(int64_t w, const int64_t* count, int chunk, int64_t* seg_
  * is row j of coeffs (t x p); codes written at column j (row stride ld). */
 int sbo_select_top(const double* coeffs, int64_t t, int p, int s0, int64_t ld, int16_t* idx,
                    double* val, void* stream);
+
+/* The coding step of sbo_code_segments (sbo.py:196-211, onb.py:170) on
+ * coefficient rows computed by sbo_coef_i8_segments: row j (p doubles) is
+ * position j < min(t, *n) (n NULL: t) of a segment table; its outputs go to
+ * column order[j] (order NULL: j) — the kept pairs (idx/val, stride ld; both
+ * NULL to skip), energy[col] = the kept score of `kind`, rest_sq[col] = the
+ * energy of the discarded coefficients (each optional).  Exact selection,
+ * ties -> lower atom. */
+int sbo_select_coded(const double* coeffs, const int64_t* n, int64_t t, int p, int s0, int kind,
+                     const int32_t* order, int64_t ld, int16_t* idx, double* val,
+                     double* energy, double* rest_sq, void* stream);
+
+/* Coefficients C = Q^T y for p = 256 (the projection of sbo_code_segments,
+ * onb.py:170) on the tcgen05 tensor cores from integer digits (tcgen05.mma
+ * kind::i8): y as the sbo_y_digits rows (p = 256, y = Y_int 2^-sy), each block
+ * entry rounded to 2^-54 in 8 digits, digit levels of weight >= 2^-49 relative
+ * kept, exact int32 sums in TMEM.  coef row t (256 float64) = the coefficients
+ * of signal order[t] (order NULL: t) in its segment's block (block_override >=
+ * 0: that block) for every position t a segment covers.  Segments as
+ * sbo_code_segments; blocks holds nblocks blocks.
+ * Workspace: sbo_coef_i8_workspace_bytes(nblocks). */
+size_t sbo_coef_i8_workspace_bytes(int nblocks);
+int sbo_coef_i8_segments(const void* ydig, int sy, const int32_t* order,
+                         const int32_t* seg_block, const int64_t* seg_lo, const int64_t* seg_hi,
+                         const int32_t* nseg, int64_t max_seg, const double* blocks, int nblocks,
+                         int block_override, double* coef, void* workspace, size_t ws_bytes,
+                         void* stream);
 
 /* ---------------------------------------------------------------------------
  * Polar update Q_b = U V^T of P_b for the blocks whose count > 0 — replaces

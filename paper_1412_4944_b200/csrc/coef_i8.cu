@@ -1,0 +1,348 @@
+// Exact float64 coefficients C = Q^T y for p = 256 (config D) on the tcgen05
+// tensor cores, from integer digits: the Ozaki split of round_i8.cu (y = Y_int
+// 2^-sy in 5 sign-magnitude 7-bit digits, each block entry rounded to 2^-54 in
+// 8 balanced digits, digit products of level <= 7 accumulated exactly in int32
+// TMEM, recombined in float64) at four times the depth and width:
+//
+// * K = 256 dims = 4 K-blocks of 64; the atoms = 4 quarters of 64.  Per
+//   128-signal tile and quarter q, the 4 K-blocks accumulate into one 512-column
+//   TMEM image (8 levels x 64 atoms, even levels in columns 0-255, odd in 256-511,
+//   exactly round_i8's layout) — |D_L| <= 5 x 256 x 127 x 64 < 2^24, and the
+//   paired levels D_L 128 + D_L+1 < 2^31 stay exact in int32.
+// * Per (quarter, K-block) stage: the tile's digit rows of the K-block (5 planes
+//   x 64 B per signal, gathered through the segment order with 16-B cp.async into
+//   the SW128 slabs [Y0|Y1] [Y2|Y3] [Y4|-]) and the block's digit image of that
+//   (quarter, K-block) (4 slabs [Q_2s|Q_2s+1] of 64 atoms x 128 B, one bulk copy).
+// * The epilogue drains a quarter (8 warps: rows 32 (w % 4), atoms 32 (w / 4)),
+//   recombines, and writes the float64 coefficients as rows of 256 at the
+//   segment position; sbo_select_top then selects on them.
+//
+// This replaces the float64 DMMA projection of the p = 256 rounds (k_code_f64);
+// the selection and the outer product stay float64.
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace sbo {
+namespace ci8 {
+
+constexpr int P = 256, TS = 128, YD = 5, QDIM = 64;
+constexpr int A_SLAB = TS * 128;     // 16 KB
+constexpr int A_BYTES = 3 * A_SLAB;  // 48 KB: one K-block of the tile's digit rows
+constexpr int B_SLAB = QDIM * 128;   // 8 KB
+constexpr int B_BYTES = 4 * B_SLAB;  // 32 KB: one (quarter, K-block) digit image
+constexpr int EPI_THREADS = 256, MMA_WARP = 8, PROD_WARP0 = 9, NPROD = 64;
+constexpr int THREADS = 352;
+constexpr int64_t QDIG_BLOCK = 16 * static_cast<int64_t>(B_BYTES);  // 512 KB per block
+
+struct Smem {
+  int8_t a[2][A_BYTES];
+  int8_t b[2][B_BYTES];
+  uint64_t full[2], empty[2], acc_full, acc_empty;
+  uint32_t tmem;
+};
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+
+__device__ __forceinline__ Smem* smem_of(unsigned char* raw) {
+  const uint32_t a = sm100::smem_u32(raw);
+  return reinterpret_cast<Smem*>(raw + ((1024u - (a & 1023u)) & 1023u));
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ uint32_t slab_off(int row, int byte) {
+  return static_cast<uint32_t>(row >> 3) * 1024u + sm100::sw128_offset(row & 7, byte);
+}
+
+__device__ __forceinline__ double l2d(long long v) {
+  const int hi = static_cast<int>(v >> 32) + 0x43380000;
+  return __hiloint2double(hi, static_cast<int>(v)) - 6755399441055744.0;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ void seg_range(int nseg, int& s0, int& s1) {
+  s0 = static_cast<int>(static_cast<int64_t>(nseg) * blockIdx.x / gridDim.x);
+  s1 = static_cast<int>(static_cast<int64_t>(nseg) * (blockIdx.x + 1) / gridDim.x);
+}
+
+struct Ring {
+  int i = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++i == 2) {
+      i = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_coef_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
+          const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
+          const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg_p,
+          const int8_t* __restrict__ qdig, int block_override, double cscale,
+          double* __restrict__ coef) {
+  extern __shared__ unsigned char raw[];
+  Smem* S = smem_of(raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nseg = *nseg_p;
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&S->full[s], NPROD);  // producer arrivals + the B bulk copy's bytes
+      sm100::mbar_init(&S->empty[s], 1);
+    }
+    sm100::mbar_init(&S->acc_full, 1);
+    sm100::mbar_init(&S->acc_empty, EPI_THREADS / 32);
+    sm100::fence_barrier_init();
+  }
+  if (warp == MMA_WARP) sm100::tmem_alloc(&S->tmem, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = S->tmem;
+  int sa, sb;
+  seg_range(nseg, sa, sb);
+  auto block_of = [&](int seg) { return block_override >= 0 ? block_override : seg_block[seg]; };
+
+  if (warp >= PROD_WARP0) {  // ------------------------------------------ producers
+    // stages in (tile, quarter, K-block) order; warp pw gathers rows
+    // [64 pw, 64 pw + 64): lane l takes 16-B chunk q = l + 32 j of each 8-row
+    // group (row q / 20, chunk q % 20: plane (q % 20) / 4, 16 B of the K-block)
+    const int pw = warp - PROD_WARP0, pt = tid - PROD_WARP0 * 32;
+    int rj[5], cj[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      rj[j] = (lane + 32 * j) / 20;
+      cj[j] = (lane + 32 * j) % 20;
+    }
+    Ring r;
+    int prev = -1;
+    for (int seg = sa; seg < sb; ++seg) {
+      const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+      const int8_t* qb = qdig + static_cast<int64_t>(block_of(seg)) * QDIG_BLOCK;
+      for (int64_t t0 = lo; t0 < hi; t0 += TS) {
+        const int n = static_cast<int>(min64(TS, hi - t0));
+        int o[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = 64 * pw + 32 * h + lane;
+          o[h] = row < n ? (order ? order[t0 + row] : static_cast<int>(t0 + row)) : 0;
+        }
+        for (int st = 0; st < 16; ++st) {  // st = 4 quarter + K-block
+          const int q = st >> 2, kb = st & 3;
+          sm100::mbar_wait(&S->empty[r.i], r.ph ^ 1u);
+          if (pt == 0) {
+            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(
+                             sm100::smem_u32(&S->full[r.i])),
+                         "r"(B_BYTES)
+                         : "memory");
+            sm100::bulk_g2s(S->b[r.i], qb + (4 * q + kb) * static_cast<int64_t>(B_BYTES),
+                            B_BYTES, &S->full[r.i]);
+          }
+          const uint32_t base = sm100::smem_u32(S->a[r.i]);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+              const int rl = 8 * g + rj[j], row = 64 * pw + rl;
+              const int sig = __shfl_sync(0xffffffffu, o[g >> 2], rl & 31);
+              const int c = cj[j], a = c >> 2;
+              cp_async16(base + (a >> 1) * A_SLAB + slab_off(row, (a & 1) * 64 + (c & 3) * 16),
+                         ydig + static_cast<int64_t>(sig) * (YD * P) + a * P + kb * QDIM +
+                             (c & 3) * 16,
+                         row < n);
+            }
+          }
+          asm volatile("cp.async.commit_group;");
+          if (prev >= 0) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            sm100::mbar_arrive(&S->full[prev]);
+          }
+          prev = r.i;
+          r.next();
+        }
+      }
+    }
+    if (prev >= 0) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sm100::mbar_arrive(&S->full[prev]);
+    }
+  } else if (warp == MMA_WARP) {  // --------------------------------------- issuer
+    if (lane == 0) {
+      Ring r;
+      uint32_t acc_ph = 0;
+      for (int seg = sa; seg < sb; ++seg) {
+        const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+        for (int64_t t0 = lo; t0 < hi; t0 += TS) {
+          for (int st = 0; st < 16; ++st) {
+            const int kb = st & 3;
+            sm100::mbar_wait(&S->full[r.i], r.ph);
+            if (kb == 0) sm100::mbar_wait(&S->acc_empty, acc_ph ^ 1u);  // quarter drained
+            sm100::tc_fence_after();
+            const uint32_t ab = sm100::smem_u32(S->a[r.i]), bb = sm100::smem_u32(S->b[r.i]);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const uint32_t ko = kk * 32;
+              const uint32_t init = (kb == 0 && kk == 0) ? 0u : 1u;
+#define CI8_MMA(A_, PI_, N_, COL_, ACC_)                                                    \
+  umma_i8(tmem + (COL_), sm100::desc_sw128(ab + ((A_) >> 1) * A_SLAB + ((A_)&1) * 64 + ko), \
+          sm100::desc_sw128(bb + (PI_)*64 + ko), idesc_i8(128, (N_)), (ACC_))
+              CI8_MMA(0, 0, 256, 0, init);    // levels 0 2 4 6
+              CI8_MMA(0, 1, 256, 256, init);  // levels 1 3 5 7
+              CI8_MMA(1, 0, 256, 256, 1u);
+              CI8_MMA(1, 1, 192, 64, 1u);
+              CI8_MMA(2, 0, 192, 64, 1u);
+              CI8_MMA(2, 1, 192, 320, 1u);
+              CI8_MMA(3, 0, 192, 320, 1u);
+              CI8_MMA(3, 1, 128, 128, 1u);
+              CI8_MMA(4, 0, 128, 128, 1u);
+              CI8_MMA(4, 1, 128, 384, 1u);
+#undef CI8_MMA
+            }
+            sm100::umma_commit(&S->empty[r.i]);
+            if (kb == 3) {
+              sm100::umma_commit(&S->acc_full);
+              acc_ph ^= 1u;
+            }
+            r.next();
+          }
+        }
+      }
+    }
+  } else {  // ------------------------------------------------------------ epilogue
+    const int q4 = warp & 3, half = warp >> 2;
+    const int row = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q4) << 16);
+    const int a0 = 32 * half;
+    uint32_t acc_ph = 0;
+    for (int seg = sa; seg < sb; ++seg) {
+      const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+      for (int64_t t0 = lo; t0 < hi; t0 += TS) {
+        const bool act = t0 + row < hi;
+        double* out = coef + (t0 + row) * P;
+        for (int q = 0; q < 4; ++q) {
+          sm100::mbar_wait(&S->acc_full, acc_ph);
+          acc_ph ^= 1u;
+          sm100::tc_fence_after();
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t v[8][8];  // [level][atom]
+#pragma unroll
+            for (int L = 0; L < 8; ++L) {
+              const uint32_t col = (L & 1 ? 256u + 64u * (L >> 1) : 64u * (L >> 1)) + a0 + 8 * ch;
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                  : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
+                    "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
+                  : "r"(lane_base + col));
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            double c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e0 = static_cast<int>(v[0][u]) * 128 + static_cast<int>(v[1][u]);
+              const int e1 = static_cast<int>(v[2][u]) * 128 + static_cast<int>(v[3][u]);
+              const int e2 = static_cast<int>(v[4][u]) * 128 + static_cast<int>(v[5][u]);
+              const int e3 = static_cast<int>(v[6][u]) * 128 + static_cast<int>(v[7][u]);
+              const double hi_ = l2d(static_cast<long long>(e0) * 16384 + e1);
+              const double lo_ = l2d(static_cast<long long>(e2) * 16384 + e3);
+              c[u] = fma(hi_, 268435456.0, lo_) * cscale;
+            }
+            if (act) {
+              double2* o2 = reinterpret_cast<double2*>(out + QDIM * q + a0 + 8 * ch);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) o2[u] = make_double2(c[2 * u], c[2 * u + 1]);
+            }
+          }
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive(&S->acc_empty);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == MMA_WARP) sm100::tmem_dealloc(tmem, 512);
+}
+
+// The block's digit images for k_coef_i8: per (quarter q, K-block kb) 32 KB =
+// 4 SW128 slabs [Q_2s | Q_2s+1] of 64 atom rows x 128 B (dims 64 kb .. + 63);
+// Q_int = rint(q 2^54) in 8 balanced 7-bit digits.  One thread per entry.
+__global__ void k_q_digits256(const double* __restrict__ blocks, int b0, int nb,
+                              int8_t* __restrict__ qdig) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= static_cast<int64_t>(nb) * P * P) return;
+  const int b = b0 + static_cast<int>(e / (P * P));
+  const int rem = static_cast<int>(e % (P * P));
+  const int dim = rem / P, atom = rem % P;  // q[dim][atom]: atom = column (numpy layout)
+  long long v = __double2ll_rn(blocks[static_cast<int64_t>(b) * P * P + rem] * 18014398509481984.0);
+  int8_t* out = qdig + static_cast<int64_t>(b) * QDIG_BLOCK +
+                (4 * (atom / QDIM) + dim / QDIM) * static_cast<int64_t>(B_BYTES);
+  const int ar = atom % QDIM, dk = dim % QDIM;
+#pragma unroll
+  for (int d = 7; d >= 0; --d) {
+    const int dd = ((static_cast<int>(v) + 64) & 127) - 64;
+    v = (v - dd) >> 7;
+    out[(d >> 1) * B_SLAB + slab_off(ar, (d & 1) * 64 + dk)] = static_cast<int8_t>(dd);
+  }
+}
+
+}  // namespace ci8
+}  // namespace sbo
+
+using namespace sbo;
+
+extern "C" size_t sbo_coef_i8_workspace_bytes(int nblocks) {
+  return static_cast<size_t>(nblocks > 0 ? nblocks : 0) * ci8::QDIG_BLOCK;
+}
+
+extern "C" int sbo_coef_i8_segments(const void* ydig, int sy, const int32_t* order,
+                                    const int32_t* seg_block, const int64_t* seg_lo,
+                                    const int64_t* seg_hi, const int32_t* nseg,
+                                    int64_t max_seg, const double* blocks, int nblocks,
+                                    int block_override, double* coef, void* workspace,
+                                    size_t ws_bytes, void* stream) {
+  if (!ydig || !blocks || !coef || nblocks < 1) return fail(SBO_EINVAL, "bad arguments");
+  if (block_override >= nblocks) return fail(SBO_EINVAL, "block_override out of range");
+  if (!workspace || ws_bytes < sbo_coef_i8_workspace_bytes(nblocks))
+    return fail(SBO_EINVAL, "coef_i8 workspace too small");
+  if (max_seg <= 0) return SBO_OK;
+  cudaStream_t st = as_stream(stream);
+  auto* qdig = static_cast<int8_t*>(workspace);
+  const int b0 = block_override >= 0 ? block_override : 0;
+  const int nb = block_override >= 0 ? 1 : nblocks;
+  const int64_t ne = static_cast<int64_t>(nb) * ci8::P * ci8::P;
+  ci8::k_q_digits256<<<static_cast<unsigned>(ceil_div(ne, 256)), 256, 0, st>>>(blocks, b0, nb,
+                                                                                qdig);
+  if (int rc = check_launch("k_q_digits256")) return rc;
+  static bool attr = false;
+  if (!attr) {
+    SBO_CHECK_CUDA(cudaFuncSetAttribute(ci8::k_coef_i8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ci8::SMEM_BYTES)));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(min64(max_seg, sms));
+  ci8::k_coef_i8<<<grid, ci8::THREADS, ci8::SMEM_BYTES, st>>>(
+      static_cast<const int8_t*>(ydig), order, seg_block, seg_lo, seg_hi, nseg, qdig,
+      block_override, ldexp(1.0, -sy - 26), coef);
+  return check_launch("k_coef_i8");
+}

@@ -406,13 +406,15 @@ __global__ void k_i8_finalize(const unsigned long long* __restrict__ acc64, int 
 }  // namespace oi8
 
 // ---------------------------------------------------------------------------
-// signal-major digit rows: row s = 5 planes x 64 dims of Y_a (y = Y_int 2^-sy,
-// Y_int = sum_a Y_a 128^(4-a), sign-magnitude), one thread per (signal, dim)
+// signal-major digit rows: row s = 5 planes x p dims of Y_a (y = Y_int 2^-sy,
+// Y_int = sum_a Y_a 128^(4-a), sign-magnitude), one thread per (signal, dim);
+// p = 64 (outer_i8.cu, round_i8.cu) or 256 (coef_i8.cu)
+template <int PD>
 __global__ void k_y_digits(const float* __restrict__ y, int64_t m, int sy, int8_t* ydig) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= m * oi8::P) return;
-  const int64_t s = e >> 6;
-  const int i = static_cast<int>(e & 63);
+  if (e >= m * PD) return;
+  const int64_t s = e / PD;
+  const int i = static_cast<int>(e % PD);
   const uint32_t bits = __float_as_uint(y[e]);
   const uint32_t ex = (bits >> 23) & 255u;
   const uint32_t mant = (bits & 0x7FFFFFu) | (ex ? 0x800000u : 0u);
@@ -428,10 +430,10 @@ __global__ void k_y_digits(const float* __restrict__ y, int64_t m, int sy, int8_
   const uint32_t d[oi8::YD] = {top, lo28 >> 21, (lo28 >> 14) & 127u, (lo28 >> 7) & 127u,
                                lo28 & 127u};
   const bool neg = bits >> 31;
-  int8_t* row = ydig + s * (oi8::YD * oi8::P);
+  int8_t* row = ydig + s * (oi8::YD * PD);
 #pragma unroll
   for (int a = 0; a < oi8::YD; ++a)
-    row[a * oi8::P + i] = static_cast<int8_t>(neg ? -static_cast<int>(d[a]) : static_cast<int>(d[a]));
+    row[a * PD + i] = static_cast<int8_t>(neg ? -static_cast<int>(d[a]) : static_cast<int>(d[a]));
 }
 
 // ---------------------------------------------------------------------------
@@ -491,11 +493,17 @@ extern "C" int sbo_i8_scan(const void* y, int dtype, int64_t m, int p, int32_t* 
 
 extern "C" int sbo_y_digits(const void* y, int dtype, int64_t m, int p, int sy, void* ydig,
                             void* stream) {
-  if (dtype != SBO_F32 || p != 64) return fail(SBO_EINVAL, "digit rows need float32, p = 64");
+  if (dtype != SBO_F32 || (p != 64 && p != 256))
+    return fail(SBO_EINVAL, "digit rows need float32, p = 64 or 256");
   if (m <= 0) return SBO_OK;
-  const int64_t n = m * 64;
-  k_y_digits<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, as_stream(stream)>>>(
-      static_cast<const float*>(y), m, sy, static_cast<int8_t*>(ydig));
+  const int64_t n = m * p;
+  const unsigned grid = static_cast<unsigned>(ceil_div(n, 256));
+  if (p == 64)
+    k_y_digits<64><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const float*>(y), m, sy,
+                                                         static_cast<int8_t*>(ydig));
+  else
+    k_y_digits<256><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const float*>(y), m, sy,
+                                                          static_cast<int8_t*>(ydig));
   return check_launch("k_y_digits");
 }
 

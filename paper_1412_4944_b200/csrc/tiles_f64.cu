@@ -841,3 +841,50 @@ extern "C" int sbo_select_top(const double* coeffs, int64_t t, int p, int s0, in
       coeffs, t, p, k, ld, idx, val);
   return check_launch("k_select_rows");
 }
+
+// The coding step of k_code_f64 (sbo.py:196-211) on coefficient rows computed
+// elsewhere (coef_i8.cu): row j is position j of a segment table whose count is
+// *n (device), its output column is order[j] (out_by_signal) or j.  Same
+// selection (pick_row, any kind), same outputs (kept pairs, score, discarded
+// energy); rows at or past *n are skipped.
+__global__ void k_select_coded(const double* __restrict__ coeffs, const int64_t* __restrict__ n,
+                               int64_t t, int p, int k, int kind,
+                               const int32_t* __restrict__ order, int64_t ld, int16_t* idx,
+                               double* val, double* energy, double* rest_sq) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
+  if (j >= t || (n && j >= *n)) return;
+  const double* Cs = coeffs + j * p;
+  const RowPick r = pick_row(Cs, p, k, kind);
+  const int64_t col = order ? order[j] : j;
+  const unsigned lt = (1u << lane) - 1u;
+  int pos = 0;
+  const int T = (p + 31) >> 5;
+  for (int q = 0; q < T; ++q) {
+    const bool on = (r.sel >> q) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (on && idx) {
+      const int at = pos + __popc(bal & lt);
+      idx[at * ld + col] = static_cast<int16_t>(lane + 32 * q);
+      val[at * ld + col] = Cs[lane + 32 * q];
+    }
+    pos += __popc(bal);
+  }
+  if (lane == 0) {
+    if (energy) energy[col] = r.score;
+    if (rest_sq) rest_sq[col] = r.rest_sq;
+  }
+}
+
+extern "C" int sbo_select_coded(const double* coeffs, const int64_t* n, int64_t t, int p, int s0,
+                                int kind, const int32_t* order, int64_t ld, int16_t* idx,
+                                double* val, double* energy, double* rest_sq, void* stream) {
+  if (p < 1 || p > kPMax) return fail(SBO_EINVAL, "p must be in [1, 256]");
+  if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
+  if (idx && !val) return fail(SBO_EINVAL, "idx without val");
+  if (t <= 0) return SBO_OK;
+  const int k = s0 < p ? s0 : p;
+  k_select_coded<<<static_cast<unsigned>(ceil_div(t, 8)), 256, 0, as_stream(stream)>>>(
+      coeffs, n, t, p, k, kind, order, ld, idx, val, energy, rest_sq);
+  return check_launch("k_select_coded");
+}

@@ -166,6 +166,7 @@ class Groups:
     seg_hi: torch.Tensor     # int64
     nseg: torch.Tensor       # int32 (1,)
     max_seg: int
+    count: torch.Tensor | None = None  # int64 (1,): positions covered (list tables)
 
     @property
     def counts(self):
@@ -223,6 +224,8 @@ class Engine:
         # tensor-core representation pass: p = 64 (tc_energy.cu) and p = 256 with
         # s0 <= 32 (tc_energy256.cu); other shapes run the float64 tile kernels
         self.i8 = None  # (sy, sx) digit scales of the tensor-core outer product
+        self.ci8 = False  # p = 256: the rounds' projection from integer digits
+        self.ysy = None   # digit scale of self.ydig (y = Y_int 2^-ysy)
         self.tc = ((self.p == 64 or (self.p == 256 and min(s0, self.p) <= 32))
                    and os.environ.get("SBO_TC", "1") != "0" and self.m > 0
                    and tc is not False)
@@ -249,9 +252,9 @@ class Engine:
                        self.stream)
         if rescan:
             self._scan_digits()
-        elif self.i8 is not None:
+        elif self.ysy is not None:
             self._call("sbo_y_digits", self.sig.y.data_ptr(), self.sig.code, self.m, self.p,
-                       self.i8[0], self.ydig.data_ptr(), self.stream)
+                       self.ysy, self.ydig.data_ptr(), self.stream)
 
     def _scan_digits(self):
         """Digit formats of the tensor-core outer product (outer_i8.cu): p = 64,
@@ -260,7 +263,9 @@ class Engine:
         float64 DMMA kernel."""
         self.i8 = None
         self.ri8 = False
-        if (self.p != 64 or self.sig.code != L.F32 or self.m == 0
+        self.ci8 = False
+        self.ysy = None
+        if (self.p not in (64, 256) or self.sig.code != L.F32 or self.m == 0
                 or os.environ.get("SBO_I8", "1") != "1"):
             return
         out = torch.empty(4, dtype=torch.int32, device=self.dev)
@@ -273,6 +278,18 @@ class Engine:
         sy = 35 - emax
         if lsb + sy < 0 or sy > 126 + 35:
             return  # some value is finer than the 35-bit grid: not exact
+        self.ysy = sy
+        if self.p == 256:
+            # p = 256: the rounds' projection from the digits (coef_i8.cu); the
+            # outer product stays float64
+            self.ci8 = os.environ.get("SBO_CI8", "1") == "1"
+            if self.ci8:
+                self.ydig = torch.empty((self.m, 5 * 256), dtype=torch.int8, device=self.dev)
+                self._call("sbo_y_digits", self.sig.y.data_ptr(), self.sig.code, self.m,
+                           self.p, sy, self.ydig.data_ptr(), self.stream)
+            else:
+                self.ysy = None
+            return
         xmax = math.sqrt(norm2) * (1.0 + 1e-6)  # |x| <= ||y|| (orthonormal blocks)
         ex = math.floor(math.log2(xmax)) + 1 if xmax > 0 else 0
         self.i8 = (sy, 54 - ex)
@@ -457,6 +474,7 @@ class Engine:
                        torch.zeros(1, dtype=torch.int32, device=self.dev), max_seg)
             self._call("sbo_chunk_segments", n, count.data_ptr(), sl, g.seg_lo.data_ptr(),
                        g.seg_hi.data_ptr(), g.nseg.data_ptr(), self.stream)
+            g.count = count
             return g
         nseg = max(1, math.ceil(n / sl)) if n > 0 else 0
         lo = torch.arange(0, max(n, 1), sl, dtype=torch.int64, device=self.dev)[:nseg]
@@ -475,6 +493,22 @@ class Engine:
                    block_override, self.s0, self.kind, int(out_by_signal), ld,
                    _ptr(idx), _ptr(val), _ptr(energy), _ptr(kept), self.stream,
                    units=self.m if order is not None and g.bounds is not None else 0)
+
+    def code_i8(self, order, g: Groups, n: int, nblocks: int, block_override: int, ld: int,
+                idx, val, energy=None, kept=None, by_signal: bool = False, count=None):
+        """``code`` for p = 256 with the projection on the tensor cores: exact
+        integer-digit coefficients of every position (coef_i8.cu), then the
+        float64 selection of sbo_code_segments on them (sbo_select_coded)."""
+        nb = block_override + 1 if block_override >= 0 else nblocks
+        ws = self.scratch.get("ci8", L.size("sbo_coef_i8_workspace_bytes", nb))
+        coef = self.scratch.get("coef", 8 * max(n, 1) * self.p)
+        self._call("sbo_coef_i8_segments", self.ydig.data_ptr(), self.ysy, _ptr(order),
+                   g.seg_block.data_ptr(), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
+                   g.nseg.data_ptr(), g.max_seg, self.blocks.data_ptr(), nb, block_override,
+                   coef.data_ptr(), ws.data_ptr(), ws.numel(), self.stream, units=n)
+        self._call("sbo_select_coded", coef.data_ptr(), _ptr(count), n, self.p, self.s0,
+                   self.kind, _ptr(order) if by_signal else None, ld, _ptr(idx), _ptr(val),
+                   _ptr(energy), _ptr(kept), self.stream, units=n)
 
     # ----------------------------------------------------------- training
     def train_rounds(self, order, g: Groups, n: int, rounds: int, nblocks: int,
@@ -535,7 +569,11 @@ class Engine:
                            self.blocks.data_ptr(), override, self.s0, partial.data_ptr(),
                            self.stream, units=n)
             else:
-                self.code(order, g, override, False, ld, idx, val)
+                if self.ci8:
+                    self.code_i8(order, g, n, nblocks, first_block if single else -1, ld,
+                                 idx, val, count=g.count)
+                else:
+                    self.code(order, g, override, False, ld, idx, val)
                 self._call("sbo_outer_segments", self.sig.y.data_ptr(), self.sig.code, p,
                            _ptr(order), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
                            g.nseg.data_ptr(), g.max_seg, self.s0, ld, idx.data_ptr(),
@@ -627,6 +665,9 @@ class Engine:
                            g.max_seg, self.blocks.data_ptr(), self.s0, self.kind,
                            self.state.residual.data_ptr(), self.state.score.data_ptr(),
                            self.stream, units=self.m)
+            elif self.ci8:
+                self.code_i8(g.perm, g, self.m, self.K, -1, max(self.m, 1), None, None,
+                             self.state.score, self.state.residual, by_signal=True)
             else:
                 ld = max(self.m, 1)
                 self.code(g.perm, g, -1, True, ld, None, None, self.state.score,
