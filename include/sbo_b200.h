@@ -321,6 +321,21 @@ int sbo_coef_i8_segments(const void* ydig, int sy, const int32_t* order,
                          int block_override, double* coef, void* workspace, size_t ws_bytes,
                          void* stream);
 
+/* The float64 re-decision of flagged signals (the role of
+ * sbo_energy_recheck_cand, same arguments and outputs) for p = 256 with the
+ * projection of sbo_coef_i8_segments: list[0 .. *nlist) sorted by candidate
+ * mask (sbo_cand_sort), cand[i] = the candidate blocks of list[i] (K <= 64);
+ * each signal's energy (sbo.py:126-135, exact selection) in each of its
+ * candidate blocks, the first maximum wins (ties -> lower block, sbo.py:191);
+ * best / score / residual of list[i] are overwritten.  ydig / sy as
+ * sbo_coef_i8_segments.  Workspace: sbo_recheck_i8_workspace_bytes(K) (for the
+ * current device). */
+size_t sbo_recheck_i8_workspace_bytes(int K);
+int sbo_energy_recheck_i8(const void* ydig, int sy, const double* blocks, int K, int s0, int kind,
+                          const int32_t* list, const uint64_t* cand, const int32_t* nlist,
+                          int64_t max_list, int32_t* best, double* score, double* residual,
+                          void* workspace, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Polar update Q_b = U V^T of P_b for the blocks whose count > 0 — replaces
  * linalg.py:68-78 (procrustes_polar via thin_svd/gesdd) and the guard of

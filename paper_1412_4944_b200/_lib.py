@@ -61,6 +61,8 @@ _SIGS = {
     "sbo_select_coded": (I, [P, P, I64, I, I, I, P, I64, P, P, P, P, P]),
     "sbo_coef_i8_workspace_bytes": (SZ, [I]),
     "sbo_coef_i8_segments": (I, [P, I, P, P, P, P, P, I64, P, I, I, P, P, SZ, P]),
+    "sbo_recheck_i8_workspace_bytes": (SZ, [I]),
+    "sbo_energy_recheck_i8": (I, [P, I, P, I, I, I, P, P, P, I64, P, P, P, P, SZ, P]),
     "sbo_polar_workspace_bytes": (SZ, [I, I]),
     "sbo_polar": (I, [P, I, I, P, P, P, P, P, P, SZ, P]),
     "sbo_init_workspace_bytes": (SZ, [I]),

@@ -20,6 +20,7 @@
 // This replaces the float64 DMMA projection of the p = 256 rounds (k_code_f64);
 // the selection and the outer product stay float64.
 #include "common.cuh"
+#include "pick.cuh"
 #include "sm100.cuh"
 
 namespace sbo {
@@ -90,17 +91,147 @@ struct Ring {
   }
 };
 
-__global__ void __launch_bounds__(THREADS, 1)
-k_coef_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
-          const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
-          const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg_p,
-          const int8_t* __restrict__ qdig, int block_override, double cscale,
-          double* __restrict__ coef) {
-  extern __shared__ unsigned char raw[];
-  Smem* S = smem_of(raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nseg = *nseg_p;
-  if (tid == 0) {
+// producers: one (quarter, K-block) stage — the block image slice by one bulk
+// copy, the tile's digit rows of the K-block by 16-B cp.async; the stage's full
+// barrier gets this warp's arrival one stage later (cp.async.wait_group 1)
+struct Producer {
+  int pw, pt, lane, rj[5], cj[5], prev = -1;
+  __device__ explicit Producer(int warp, int tid) {
+    pw = warp - PROD_WARP0;
+    pt = tid - PROD_WARP0 * 32;
+    lane = tid & 31;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      rj[j] = (lane + 32 * j) / 20;
+      cj[j] = (lane + 32 * j) % 20;
+    }
+  }
+  // warp pw gathers rows [64 pw, 64 pw + 64): lane l takes 16-B chunk
+  // c = l + 32 j of each 8-row group (row c / 20, plane (c % 20) / 4)
+  __device__ __forceinline__ void stage(Smem* S, Ring& r, const int8_t* qimg,
+                                        const int8_t* __restrict__ ydig, const int (&o)[2], int n,
+                                        int kb) {
+    sm100::mbar_wait(&S->empty[r.i], r.ph ^ 1u);
+    if (pt == 0) {
+      asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(
+                       sm100::smem_u32(&S->full[r.i])),
+                   "r"(B_BYTES)
+                   : "memory");
+      sm100::bulk_g2s(S->b[r.i], qimg, B_BYTES, &S->full[r.i]);
+    }
+    const uint32_t base = sm100::smem_u32(S->a[r.i]);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const int rl = 8 * g + rj[j], row = 64 * pw + rl;
+        const int sig = __shfl_sync(0xffffffffu, o[g >> 2], rl & 31);
+        const int c = cj[j], a = c >> 2;
+        cp_async16(base + (a >> 1) * A_SLAB + slab_off(row, (a & 1) * 64 + (c & 3) * 16),
+                   ydig + static_cast<int64_t>(sig) * (YD * P) + a * P + kb * QDIM + (c & 3) * 16,
+                   row < n);
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+    if (prev >= 0) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sm100::mbar_arrive(&S->full[prev]);
+    }
+    prev = r.i;
+    r.next();
+  }
+  __device__ __forceinline__ void finish(Smem* S) {
+    if (prev >= 0) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sm100::mbar_arrive(&S->full[prev]);
+    }
+  }
+};
+
+// issuer (one thread): the 10 digit-pair MMAs of both 32-deep k-steps of a
+// stage; a quarter's accumulators are initialised at K-block 0 (after the
+// epilogue drained the previous quarter) and committed after K-block 3
+__device__ __forceinline__ void mma_stage(Smem* S, uint32_t tmem, Ring& r, int kb,
+                                          uint32_t& acc_ph) {
+  sm100::mbar_wait(&S->full[r.i], r.ph);
+  if (kb == 0) sm100::mbar_wait(&S->acc_empty, acc_ph ^ 1u);
+  sm100::tc_fence_after();
+  const uint32_t ab = sm100::smem_u32(S->a[r.i]), bb = sm100::smem_u32(S->b[r.i]);
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+    const uint32_t ko = kk * 32;
+    const uint32_t init = (kb == 0 && kk == 0) ? 0u : 1u;
+    // (y digit A_, Q parity PI_, N, TMEM column): levels A_ + PI_ + 2i of one parity
+#define CI8_MMA(A_, PI_, N_, COL_, ACC_)                                                    \
+  umma_i8(tmem + (COL_), sm100::desc_sw128(ab + ((A_) >> 1) * A_SLAB + ((A_)&1) * 64 + ko), \
+          sm100::desc_sw128(bb + (PI_)*64 + ko), idesc_i8(128, (N_)), (ACC_))
+    CI8_MMA(0, 0, 256, 0, init);    // levels 0 2 4 6
+    CI8_MMA(0, 1, 256, 256, init);  // levels 1 3 5 7
+    CI8_MMA(1, 0, 256, 256, 1u);
+    CI8_MMA(1, 1, 192, 64, 1u);
+    CI8_MMA(2, 0, 192, 64, 1u);
+    CI8_MMA(2, 1, 192, 320, 1u);
+    CI8_MMA(3, 0, 192, 320, 1u);
+    CI8_MMA(3, 1, 128, 128, 1u);
+    CI8_MMA(4, 0, 128, 128, 1u);
+    CI8_MMA(4, 1, 128, 384, 1u);
+#undef CI8_MMA
+  }
+  sm100::umma_commit(&S->empty[r.i]);
+  if (kb == 3) {
+    sm100::umma_commit(&S->acc_full);
+    acc_ph ^= 1u;
+  }
+  r.next();
+}
+
+// epilogue warp: one quarter's 32 atoms (a0 ..) of its 32 rows out of TMEM,
+// recombined to float64 and stored at out[64 q + a0 ..] (out NULL: discarded)
+__device__ __forceinline__ void drain_quarter(Smem* S, uint32_t lane_base, int a0, int q,
+                                              uint32_t& acc_ph, double cscale, double* out) {
+  const int lane = threadIdx.x & 31;
+  sm100::mbar_wait(&S->acc_full, acc_ph);
+  acc_ph ^= 1u;
+  sm100::tc_fence_after();
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t v[8][8];  // [level][atom]
+#pragma unroll
+    for (int L = 0; L < 8; ++L) {
+      const uint32_t col = (L & 1 ? 256u + 64u * (L >> 1) : 64u * (L >> 1)) + a0 + 8 * ch;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
+            "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
+          : "r"(lane_base + col));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    double c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e0 = static_cast<int>(v[0][u]) * 128 + static_cast<int>(v[1][u]);
+      const int e1 = static_cast<int>(v[2][u]) * 128 + static_cast<int>(v[3][u]);
+      const int e2 = static_cast<int>(v[4][u]) * 128 + static_cast<int>(v[5][u]);
+      const int e3 = static_cast<int>(v[6][u]) * 128 + static_cast<int>(v[7][u]);
+      const double hi_ = l2d(static_cast<long long>(e0) * 16384 + e1);
+      const double lo_ = l2d(static_cast<long long>(e2) * 16384 + e3);
+      c[u] = fma(hi_, 268435456.0, lo_) * cscale;
+    }
+    if (out) {
+      double2* o2 = reinterpret_cast<double2*>(out + QDIM * q + a0 + 8 * ch);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o2[u] = make_double2(c[2 * u], c[2 * u + 1]);
+    }
+  }
+  sm100::tc_fence_before();
+  __syncwarp();
+  if (lane == 0) sm100::mbar_arrive(&S->acc_empty);
+}
+
+__device__ __forceinline__ void setup(Smem* S, int warp) {
+  if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&S->full[s], NPROD);  // producer arrivals + the B bulk copy's bytes
       sm100::mbar_init(&S->empty[s], 1);
@@ -113,24 +244,27 @@ k_coef_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_coef_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
+          const int32_t* __restrict__ seg_block, const int64_t* __restrict__ seg_lo,
+          const int64_t* __restrict__ seg_hi, const int32_t* __restrict__ nseg_p,
+          const int8_t* __restrict__ qdig, int block_override, double cscale,
+          double* __restrict__ coef) {
+  extern __shared__ unsigned char raw[];
+  Smem* S = smem_of(raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nseg = *nseg_p;
+  setup(S, warp);
   const uint32_t tmem = S->tmem;
   int sa, sb;
   seg_range(nseg, sa, sb);
   auto block_of = [&](int seg) { return block_override >= 0 ? block_override : seg_block[seg]; };
 
   if (warp >= PROD_WARP0) {  // ------------------------------------------ producers
-    // stages in (tile, quarter, K-block) order; warp pw gathers rows
-    // [64 pw, 64 pw + 64): lane l takes 16-B chunk q = l + 32 j of each 8-row
-    // group (row q / 20, chunk q % 20: plane (q % 20) / 4, 16 B of the K-block)
-    const int pw = warp - PROD_WARP0, pt = tid - PROD_WARP0 * 32;
-    int rj[5], cj[5];
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      rj[j] = (lane + 32 * j) / 20;
-      cj[j] = (lane + 32 * j) % 20;
-    }
+    Producer pr(warp, tid);
     Ring r;
-    int prev = -1;
     for (int seg = sa; seg < sb; ++seg) {
       const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
       const int8_t* qb = qdig + static_cast<int64_t>(block_of(seg)) * QDIG_BLOCK;
@@ -139,140 +273,149 @@ k_coef_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         int o[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int row = 64 * pw + 32 * h + lane;
+          const int row = 64 * pr.pw + 32 * h + lane;
           o[h] = row < n ? (order ? order[t0 + row] : static_cast<int>(t0 + row)) : 0;
         }
-        for (int st = 0; st < 16; ++st) {  // st = 4 quarter + K-block
-          const int q = st >> 2, kb = st & 3;
-          sm100::mbar_wait(&S->empty[r.i], r.ph ^ 1u);
-          if (pt == 0) {
-            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(
-                             sm100::smem_u32(&S->full[r.i])),
-                         "r"(B_BYTES)
-                         : "memory");
-            sm100::bulk_g2s(S->b[r.i], qb + (4 * q + kb) * static_cast<int64_t>(B_BYTES),
-                            B_BYTES, &S->full[r.i]);
-          }
-          const uint32_t base = sm100::smem_u32(S->a[r.i]);
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-#pragma unroll
-            for (int j = 0; j < 5; ++j) {
-              const int rl = 8 * g + rj[j], row = 64 * pw + rl;
-              const int sig = __shfl_sync(0xffffffffu, o[g >> 2], rl & 31);
-              const int c = cj[j], a = c >> 2;
-              cp_async16(base + (a >> 1) * A_SLAB + slab_off(row, (a & 1) * 64 + (c & 3) * 16),
-                         ydig + static_cast<int64_t>(sig) * (YD * P) + a * P + kb * QDIM +
-                             (c & 3) * 16,
-                         row < n);
-            }
-          }
-          asm volatile("cp.async.commit_group;");
-          if (prev >= 0) {
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            sm100::mbar_arrive(&S->full[prev]);
-          }
-          prev = r.i;
-          r.next();
-        }
+        for (int st = 0; st < 16; ++st)  // st = 4 quarter + K-block
+          pr.stage(S, r, qb + st * static_cast<int64_t>(B_BYTES), ydig, o, n, st & 3);
       }
     }
-    if (prev >= 0) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      sm100::mbar_arrive(&S->full[prev]);
-    }
+    pr.finish(S);
   } else if (warp == MMA_WARP) {  // --------------------------------------- issuer
     if (lane == 0) {
       Ring r;
       uint32_t acc_ph = 0;
       for (int seg = sa; seg < sb; ++seg) {
         const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
-        for (int64_t t0 = lo; t0 < hi; t0 += TS) {
-          for (int st = 0; st < 16; ++st) {
-            const int kb = st & 3;
-            sm100::mbar_wait(&S->full[r.i], r.ph);
-            if (kb == 0) sm100::mbar_wait(&S->acc_empty, acc_ph ^ 1u);  // quarter drained
-            sm100::tc_fence_after();
-            const uint32_t ab = sm100::smem_u32(S->a[r.i]), bb = sm100::smem_u32(S->b[r.i]);
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              const uint32_t ko = kk * 32;
-              const uint32_t init = (kb == 0 && kk == 0) ? 0u : 1u;
-#define CI8_MMA(A_, PI_, N_, COL_, ACC_)                                                    \
-  umma_i8(tmem + (COL_), sm100::desc_sw128(ab + ((A_) >> 1) * A_SLAB + ((A_)&1) * 64 + ko), \
-          sm100::desc_sw128(bb + (PI_)*64 + ko), idesc_i8(128, (N_)), (ACC_))
-              CI8_MMA(0, 0, 256, 0, init);    // levels 0 2 4 6
-              CI8_MMA(0, 1, 256, 256, init);  // levels 1 3 5 7
-              CI8_MMA(1, 0, 256, 256, 1u);
-              CI8_MMA(1, 1, 192, 64, 1u);
-              CI8_MMA(2, 0, 192, 64, 1u);
-              CI8_MMA(2, 1, 192, 320, 1u);
-              CI8_MMA(3, 0, 192, 320, 1u);
-              CI8_MMA(3, 1, 128, 128, 1u);
-              CI8_MMA(4, 0, 128, 128, 1u);
-              CI8_MMA(4, 1, 128, 384, 1u);
-#undef CI8_MMA
-            }
-            sm100::umma_commit(&S->empty[r.i]);
-            if (kb == 3) {
-              sm100::umma_commit(&S->acc_full);
-              acc_ph ^= 1u;
-            }
-            r.next();
-          }
-        }
+        for (int64_t t0 = lo; t0 < hi; t0 += TS)
+          for (int st = 0; st < 16; ++st) mma_stage(S, tmem, r, st & 3, acc_ph);
       }
     }
   } else {  // ------------------------------------------------------------ epilogue
-    const int q4 = warp & 3, half = warp >> 2;
+    const int q4 = warp & 3;
     const int row = 32 * q4 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q4) << 16);
-    const int a0 = 32 * half;
+    const int a0 = 32 * (warp >> 2);
     uint32_t acc_ph = 0;
     for (int seg = sa; seg < sb; ++seg) {
       const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
       for (int64_t t0 = lo; t0 < hi; t0 += TS) {
-        const bool act = t0 + row < hi;
-        double* out = coef + (t0 + row) * P;
-        for (int q = 0; q < 4; ++q) {
-          sm100::mbar_wait(&S->acc_full, acc_ph);
-          acc_ph ^= 1u;
-          sm100::tc_fence_after();
+        double* out = t0 + row < hi ? coef + (t0 + row) * P : nullptr;
+        for (int q = 0; q < 4; ++q) drain_quarter(S, lane_base, a0, q, acc_ph, cscale, out);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == MMA_WARP) sm100::tmem_dealloc(tmem, 512);
+}
+
+// union of the candidate masks of a tile's rows (every lane of the warp calls it)
+__device__ __forceinline__ uint64_t tile_union(const uint64_t* __restrict__ cand, int64_t base,
+                                               int n) {
+  uint64_t u = 0;
+  for (int i = threadIdx.x & 31; i < n; i += 32) u |= cand[base + i];
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(u));
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(u >> 32));
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// The float64 re-decision of the signals the tensor-core energy pass flagged
+// (sbo.py:177-194 over each signal's candidate blocks; the role of
+// sbo_energy_recheck_cand, tiles_f64.cu): tiles of 128 flagged signals (sorted by
+// candidate mask, so a tile's masks mostly agree); for each block of the tile's
+// union, the exact digit projection of the tile as above, its four quarters
+// drained to a per-CTA float64 row buffer (L2-resident, double-buffered across
+// blocks), then each epilogue warp ranks its rows whose mask holds the block
+// (pick_row, the exact selection) and keeps the first maximum (blocks ascending:
+// ties -> lower block, sbo.py:191).
+__global__ void __launch_bounds__(THREADS, 1)
+k_recheck_i8(const int8_t* __restrict__ ydig, const int32_t* __restrict__ list,
+             const uint64_t* __restrict__ cand, const int32_t* __restrict__ nlist,
+             const int8_t* __restrict__ qdig, int k, int kind, double cscale, double* scratch,
+             int32_t* best, double* score, double* residual) {
+  extern __shared__ unsigned char raw[];
+  Smem* S = smem_of(raw);
+  __shared__ double bscore[TS], brest[TS];
+  __shared__ int bbest[TS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t count = *nlist;
+  const int64_t ntiles = (count + TS - 1) / TS;
+  setup(S, warp);
+  const uint32_t tmem = S->tmem;
+
+  if (warp >= PROD_WARP0) {  // ------------------------------------------ producers
+    Producer pr(warp, tid);
+    Ring r;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t t0 = tile * TS;
+      const int n = static_cast<int>(min64(TS, count - t0));
+      int o[2];
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t v[8][8];  // [level][atom]
-#pragma unroll
-            for (int L = 0; L < 8; ++L) {
-              const uint32_t col = (L & 1 ? 256u + 64u * (L >> 1) : 64u * (L >> 1)) + a0 + 8 * ch;
-              asm volatile(
-                  "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                  : "=r"(v[L][0]), "=r"(v[L][1]), "=r"(v[L][2]), "=r"(v[L][3]), "=r"(v[L][4]),
-                    "=r"(v[L][5]), "=r"(v[L][6]), "=r"(v[L][7])
-                  : "r"(lane_base + col));
-            }
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            double c[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int e0 = static_cast<int>(v[0][u]) * 128 + static_cast<int>(v[1][u]);
-              const int e1 = static_cast<int>(v[2][u]) * 128 + static_cast<int>(v[3][u]);
-              const int e2 = static_cast<int>(v[4][u]) * 128 + static_cast<int>(v[5][u]);
-              const int e3 = static_cast<int>(v[6][u]) * 128 + static_cast<int>(v[7][u]);
-              const double hi_ = l2d(static_cast<long long>(e0) * 16384 + e1);
-              const double lo_ = l2d(static_cast<long long>(e2) * 16384 + e3);
-              c[u] = fma(hi_, 268435456.0, lo_) * cscale;
-            }
-            if (act) {
-              double2* o2 = reinterpret_cast<double2*>(out + QDIM * q + a0 + 8 * ch);
-#pragma unroll
-              for (int u = 0; u < 4; ++u) o2[u] = make_double2(c[2 * u], c[2 * u + 1]);
-            }
+      for (int h = 0; h < 2; ++h) {
+        const int row = 64 * pr.pw + 32 * h + lane;
+        o[h] = row < n ? list[t0 + row] : 0;
+      }
+      for (uint64_t u = tile_union(cand, t0, n); u; u &= u - 1) {
+        const int8_t* qb = qdig + static_cast<int64_t>(__ffsll(u) - 1) * QDIG_BLOCK;
+        for (int st = 0; st < 16; ++st)
+          pr.stage(S, r, qb + st * static_cast<int64_t>(B_BYTES), ydig, o, n, st & 3);
+      }
+    }
+    pr.finish(S);
+  } else if (warp == MMA_WARP) {  // --------------------------------------- issuer
+    Ring r;
+    uint32_t acc_ph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t t0 = tile * TS;
+      const int n = static_cast<int>(min64(TS, count - t0));
+      const int nb = __popcll(tile_union(cand, t0, n));
+      if (lane == 0)
+        for (int i = 0; i < 16 * nb; ++i) mma_stage(S, tmem, r, i & 3, acc_ph);
+      __syncwarp();
+    }
+  } else {  // ------------------------------------------------------------ epilogue
+    const int q4 = warp & 3;
+    const int row = 32 * q4 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q4) << 16);
+    const int a0 = 32 * (warp >> 2);
+    uint32_t acc_ph = 0;
+    int buf = 0;
+    double* scr = scratch + static_cast<int64_t>(blockIdx.x) * 2 * TS * P;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t t0 = tile * TS;
+      const int n = static_cast<int>(min64(TS, count - t0));
+      for (int rr = warp; rr < TS; rr += EPI_THREADS / 32) {  // this warp's selection rows
+        if (lane == 0) {
+          bscore[rr] = -1.0;
+          brest[rr] = 0.0;
+          bbest[rr] = -1;
+        }
+      }
+      for (uint64_t u = tile_union(cand, t0, n); u; u &= u - 1) {
+        const int b = __ffsll(u) - 1;
+        double* rows = scr + buf * TS * P;
+        for (int q = 0; q < 4; ++q)
+          drain_quarter(S, lane_base, a0, q, acc_ph, cscale, row < n ? rows + row * P : nullptr);
+        __threadfence_block();
+        asm volatile("bar.sync 1, %0;" ::"r"(EPI_THREADS) : "memory");
+        for (int rr = warp; rr < n; rr += EPI_THREADS / 32) {
+          if (!((cand[t0 + rr] >> b) & 1ull)) continue;
+          const RowPick pk = pick_row(rows + rr * P, P, k, kind);
+          if (lane == 0 && pk.score > bscore[rr]) {  // strict: first maximum wins
+            bscore[rr] = pk.score;
+            brest[rr] = pk.rest_sq;
+            bbest[rr] = b;
           }
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&S->acc_empty);
+        }
+        buf ^= 1;
+      }
+      __syncwarp();
+      for (int rr = warp; rr < n; rr += EPI_THREADS / 32) {
+        if (lane == 0) {
+          const int64_t j = list[t0 + rr];
+          best[j] = bbest[rr];
+          score[j] = bscore[rr];
+          residual[j] = brest[rr];
         }
       }
     }
@@ -308,6 +451,15 @@ __global__ void k_q_digits256(const double* __restrict__ blocks, int b0, int nb,
 
 using namespace sbo;
 
+namespace {
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+}  // namespace
+
 extern "C" size_t sbo_coef_i8_workspace_bytes(int nblocks) {
   return static_cast<size_t>(nblocks > 0 ? nblocks : 0) * ci8::QDIG_BLOCK;
 }
@@ -337,12 +489,50 @@ extern "C" int sbo_coef_i8_segments(const void* ydig, int sy, const int32_t* ord
                                         static_cast<int>(ci8::SMEM_BYTES)));
     attr = true;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = static_cast<unsigned>(min64(max_seg, sms));
+  const unsigned grid = static_cast<unsigned>(min64(max_seg, sm_count()));
   ci8::k_coef_i8<<<grid, ci8::THREADS, ci8::SMEM_BYTES, st>>>(
       static_cast<const int8_t*>(ydig), order, seg_block, seg_lo, seg_hi, nseg, qdig,
       block_override, ldexp(1.0, -sy - 26), coef);
   return check_launch("k_coef_i8");
+}
+
+extern "C" size_t sbo_recheck_i8_workspace_bytes(int K) {
+  return static_cast<size_t>(K > 0 ? K : 0) * ci8::QDIG_BLOCK +
+         static_cast<size_t>(sm_count()) * 2 * ci8::TS * ci8::P * sizeof(double);
+}
+
+extern "C" int sbo_energy_recheck_i8(const void* ydig, int sy, const double* blocks, int K,
+                                     int s0, int kind, const int32_t* list,
+                                     const uint64_t* cand, const int32_t* nlist,
+                                     int64_t max_list, int32_t* best, double* score,
+                                     double* residual, void* workspace, size_t ws_bytes,
+                                     void* stream) {
+  if (!ydig || !blocks || !list || !cand || !nlist || !best || !score || !residual)
+    return fail(SBO_EINVAL, "bad arguments");
+  if (K < 1 || K > 64) return fail(SBO_EINVAL, "the candidate recheck needs 1 <= K <= 64");
+  if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
+  if (!workspace || ws_bytes < sbo_recheck_i8_workspace_bytes(K))
+    return fail(SBO_EINVAL, "recheck_i8 workspace too small");
+  if (max_list <= 0) return SBO_OK;
+  cudaStream_t st = as_stream(stream);
+  auto* qdig = static_cast<int8_t*>(workspace);
+  const int64_t ne = static_cast<int64_t>(K) * ci8::P * ci8::P;
+  ci8::k_q_digits256<<<static_cast<unsigned>(ceil_div(ne, 256)), 256, 0, st>>>(blocks, 0, K,
+                                                                                qdig);
+  if (int rc = check_launch("k_q_digits256")) return rc;
+  static bool attr = false;
+  if (!attr) {
+    SBO_CHECK_CUDA(cudaFuncSetAttribute(ci8::k_recheck_i8,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ci8::SMEM_BYTES)));
+    attr = true;
+  }
+  const int sms = sm_count();
+  const unsigned grid =
+      static_cast<unsigned>(min64(ceil_div(max_list, static_cast<int64_t>(ci8::TS)), sms));
+  auto* scratch = reinterpret_cast<double*>(qdig + K * ci8::QDIG_BLOCK);
+  ci8::k_recheck_i8<<<grid, ci8::THREADS, ci8::SMEM_BYTES, st>>>(
+      static_cast<const int8_t*>(ydig), list, cand, nlist, qdig, s0 < ci8::P ? s0 : ci8::P, kind,
+      ldexp(1.0, -sy - 26), scratch, best, score, residual);
+  return check_launch("k_recheck_i8");
 }

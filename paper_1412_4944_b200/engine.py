@@ -416,11 +416,21 @@ class Engine:
                 self._call("sbo_cand_sort", self.flags.data_ptr(), self.cand.data_ptr(),
                            self.nflag.data_ptr(), self.m, self.flags_sorted.data_ptr(),
                            self.cand_sorted.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
-                self._call("sbo_energy_recheck_cand", self.sig.y.data_ptr(), self.sig.code,
-                           self.m, self.p, self.blocks.data_ptr(), b1, self.s0, self.kind,
-                           self.flags_sorted.data_ptr(), self.cand_sorted.data_ptr(),
-                           self.nflag.data_ptr(), self.m, s.best.data_ptr(),
-                           s.score.data_ptr(), s.residual.data_ptr(), self.stream)
+                if self.ci8:  # p = 256: the projection from the integer digits
+                    ws = self.scratch.get("rci8", L.size("sbo_recheck_i8_workspace_bytes", b1))
+                    self._call("sbo_energy_recheck_i8", self.ydig.data_ptr(), self.ysy,
+                               self.blocks.data_ptr(), b1, self.s0, self.kind,
+                               self.flags_sorted.data_ptr(), self.cand_sorted.data_ptr(),
+                               self.nflag.data_ptr(), self.m, s.best.data_ptr(),
+                               s.score.data_ptr(), s.residual.data_ptr(), ws.data_ptr(),
+                               ws.numel(), self.stream)
+                else:
+                    self._call("sbo_energy_recheck_cand", self.sig.y.data_ptr(),
+                               self.sig.code, self.m, self.p, self.blocks.data_ptr(), b1,
+                               self.s0, self.kind, self.flags_sorted.data_ptr(),
+                               self.cand_sorted.data_ptr(), self.nflag.data_ptr(), self.m,
+                               s.best.data_ptr(), s.score.data_ptr(), s.residual.data_ptr(),
+                               self.stream)
             else:
                 # more than 64 blocks: the flagged signals are re-decided over every
                 # block from scratch

@@ -188,3 +188,39 @@ def test_iteration_ci8_matches_dmma(dev, monkeypatch):
     assert np.abs(b1 - b0).max() < 1e-11
     assert np.abs(r1 - r0).max() <= 1e-12 * max(r0.max(), 1e-300)
     assert abs(e1 - e0) <= 1e-12 * e0
+
+
+@pytest.mark.parametrize("kind", ["squared-sum", "abs-sum"])
+def test_recheck_i8_near_tied_blocks_match_oracle(dev, kind, monkeypatch):
+    """Perturbed copies of the signals' principal basis: every signal's
+    energies are within the tensor-core certificate in several blocks, so most
+    signals go to the float64 re-decision (sbo_energy_recheck_i8) with
+    multi-block candidate masks.  Decisions equal the oracle's; the float64 one
+    through the DMMA recheck gives the same state."""
+    rows = signals.patch_signals(3000, 16, 512, 512)
+    # only near-copies compete
+    base = np.linalg.eigh(rows.T.astype(np.float64) @ rows.astype(np.float64))[1][:, ::-1]
+    qs = [np.ascontiguousarray(base)]
+    rng = np.random.default_rng(21)
+    for i in range(5):  # perturbed copies: energies 1e-8 .. 1e-7 apart, no exact ties
+        q, r = np.linalg.qr(base + 2e-8 * (i + 1) * rng.standard_normal((P, P)))
+        qs.append(q * np.sign(np.diag(r)))
+    states = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SBO_CI8", flag)
+        eng = Engine(Signals.from_rows(rows, dev), 16, kind, k_cap=len(qs))
+        eng.set_blocks(np.stack(qs))
+        assert eng.ci8 == (flag == "1")
+        eng.energy(0, eng.K, False)
+        torch.cuda.synchronize()
+        assert int(eng.nflag.item()) > 1000  # the re-decision is exercised
+        st = eng.state
+        states.append((st.best.cpu().numpy(), st.score.cpu().numpy(),
+                       st.residual.cpu().numpy()))
+    r = O.code_signals(rows.T.astype(np.float64), qs, 16, kind)
+    (b1, s1, r1), (b0, s0_, r0) = states
+    np.testing.assert_array_equal(b1, r.block)
+    np.testing.assert_array_equal(b0, r.block)
+    n2 = (rows.astype(np.float64) ** 2).sum(1)
+    assert (np.abs(s1 - s0_) <= 1e-13 * n2 + 1e-300).all()
+    assert (np.abs(r1 - r0) <= 1e-13 * n2 + 1e-300).all()
