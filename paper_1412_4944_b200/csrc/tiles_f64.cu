@@ -511,6 +511,117 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
   }
 }
 
+// Sparse outer products for p = 256 (config D), k <= 32 kept atoms per signal:
+// P[d][a] = sum over the segment's signals of y[d] x[a], on the CUDA cores in
+// float64 with only the kept pairs multiplied (k / p = 1/16 of the dense DMMA
+// product's work).  CTA (segment, dim quarter): 16 warps, warp w owns atoms
+// w + 16 j, lane the dims 64 q + 2 lane + {0, 1} — 32 float64 accumulators in
+// registers.  Per chunk of 64 signals: the quarter's y rows as float64 and the
+// codes densified per atom in shared memory with a 64-bit signal mask per atom
+// (atomicOr: order-free); each warp walks its atoms' masks in ascending signal
+// order, so the summation order — and the partial — is deterministic.  The next
+// chunk's y and codes are prefetched into registers during the FMAs.
+namespace osp {
+constexpr int P = 256, DQ = 64, C = 64, THREADS = 512, WARPS = 16, AW = P / WARPS;
+constexpr int KMAX = 32, CODES = C * KMAX / THREADS;  // code entries per thread
+struct Smem {
+  double ys[C][DQ];
+  double xval[P][C];
+  uint32_t mask[2][P][C / 32];
+};
+}  // namespace osp
+
+template <typename TY>
+__global__ void __launch_bounds__(osp::THREADS, 1) k_outer_sparse256(
+    const TY* __restrict__ y, const int32_t* __restrict__ order,
+    const int64_t* __restrict__ seg_lo, const int64_t* __restrict__ seg_hi,
+    const int32_t* __restrict__ nseg, int k, int64_t ld, const int16_t* __restrict__ idx,
+    const double* __restrict__ val, double* partial) {
+  using namespace osp;
+  if (static_cast<int>(blockIdx.x) >= *nseg) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  Smem& S = *reinterpret_cast<Smem*>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int seg = blockIdx.x, d0 = DQ * static_cast<int>(blockIdx.y);
+  const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
+  reinterpret_cast<uint32_t*>(S.mask)[tid] = 0u;  // both mask buffers: 2 x 256 x 2 words
+  reinterpret_cast<uint32_t*>(S.mask)[tid + THREADS] = 0u;
+  // prefetch: y row tid / 8, dims d0 + 8 (tid % 8) .. + 7; code entries e = tid + 512 i
+  // (signal e % 64, slot e / 64)
+  const int yr = tid >> 3, yc = 8 * (tid & 7);
+  double yv[8];
+  int ci[CODES];
+  double cv[CODES];
+  auto prefetch = [&](int64_t t0) {
+    const int64_t t = t0 + yr;
+    if (t < hi) {
+      const int64_t r = order ? static_cast<int64_t>(order[t]) : t;
+      const TY* src = y + r * P + d0 + yc;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) yv[i] = static_cast<double>(__ldg(src + i));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) yv[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < CODES; ++i) {
+      const int e = tid + THREADS * i, s = e % C, u = e / C;
+      const int64_t col = t0 + s;
+      ci[i] = -1;
+      if (u < k && col < hi) {
+        ci[i] = idx[u * ld + col];
+        cv[i] = val[u * ld + col];
+      }
+    }
+  };
+  double acc[AW][2];
+#pragma unroll
+  for (int j = 0; j < AW; ++j) acc[j][0] = acc[j][1] = 0.0;
+  int buf = 0;
+  if (lo < hi) prefetch(lo);
+  __syncthreads();
+  for (int64_t t0 = lo; t0 < hi; t0 += C) {
+    // stage the prefetched chunk (the previous chunk's FMAs are done: sync below)
+#pragma unroll
+    for (int i = 0; i < 8; i += 2)
+      *reinterpret_cast<double2*>(&S.ys[yr][yc + i]) = make_double2(yv[i], yv[i + 1]);
+#pragma unroll
+    for (int i = 0; i < CODES; ++i) {
+      if (ci[i] >= 0) {
+        const int s = (tid + THREADS * i) % C;
+        S.xval[ci[i]][s] = cv[i];
+        atomicOr(&S.mask[buf][ci[i]][s >> 5], 1u << (s & 31));
+      }
+    }
+    __syncthreads();
+    if (t0 + C < hi) prefetch(t0 + C);
+    reinterpret_cast<uint32_t*>(S.mask[buf ^ 1])[tid] = 0u;  // the next chunk's masks
+#pragma unroll
+    for (int j = 0; j < AW; ++j) {
+      const int a = warp + WARPS * j;
+#pragma unroll
+      for (int w = 0; w < C / 32; ++w) {
+        for (uint32_t m = S.mask[buf][a][w]; m; m &= m - 1) {
+          const int s = 32 * w + __ffs(m) - 1;
+          const double x = S.xval[a][s];
+          const double2 yy = *reinterpret_cast<const double2*>(&S.ys[s][2 * lane]);
+          acc[j][0] = fma(yy.x, x, acc[j][0]);
+          acc[j][1] = fma(yy.y, x, acc[j][1]);
+        }
+      }
+    }
+    buf ^= 1;
+    __syncthreads();
+  }
+  double* out = partial + static_cast<int64_t>(seg) * P * P;
+#pragma unroll
+  for (int j = 0; j < AW; ++j) {
+    const int a = warp + WARPS * j;
+    out[static_cast<int64_t>(d0 + 2 * lane) * P + a] = acc[j][0];
+    out[static_cast<int64_t>(d0 + 2 * lane + 1) * P + a] = acc[j][1];
+  }
+}
+
 // P_b = sum of block b's segment partials.  A CTA owns 32 consecutive elements;
 // its 8 warps take the segments s0 + w, s0 + w + 8, ... (coalesced 256-B rows),
 // and the 8 slice sums are added in slice order: a fixed summation order, so the
@@ -647,6 +758,14 @@ int outer_impl(const void* yv, int p, const int32_t* order, const int64_t* seg_l
                const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg, int k, int64_t ld,
                const int16_t* idx, const double* val, int dense_self, double* partial,
                cudaStream_t st) {
+  if (p == osp::P && !dense_self && k <= osp::KMAX) {
+    cudaFuncSetAttribute(k_outer_sparse256<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(osp::Smem)));
+    k_outer_sparse256<TY><<<dim3(static_cast<unsigned>(max_seg), osp::P / osp::DQ),
+                            osp::THREADS, sizeof(osp::Smem), st>>>(
+        static_cast<const TY*>(yv), order, seg_lo, seg_hi, nseg, k, ld, idx, val, partial);
+    return check_launch("k_outer_sparse256");
+  }
   const OuterLayout L;
   cudaFuncSetAttribute(k_outer_f64<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(L.bytes));
