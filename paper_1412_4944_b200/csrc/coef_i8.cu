@@ -27,8 +27,9 @@ namespace sbo {
 namespace ci8 {
 
 constexpr int P = 256, TS = 128, YD = 5, QDIM = 64;
-constexpr int A_SLAB = TS * 128;     // 16 KB
-constexpr int A_BYTES = 3 * A_SLAB;  // 48 KB: one K-block of the tile's digit rows
+constexpr int A_SLAB = TS * 128;               // 16 KB: [Y_2j | Y_2j+1], 128-B swizzle
+constexpr int A_BYTES = 2 * A_SLAB + TS * 64;  // 40 KB: + Y4 alone, 64-B swizzle
+constexpr int NST = 3;                         // pipeline stages
 constexpr int B_SLAB = QDIM * 128;   // 8 KB
 constexpr int B_BYTES = 4 * B_SLAB;  // 32 KB: one (quarter, K-block) digit image
 constexpr int EPI_THREADS = 256, MMA_WARP = 8, PROD_WARP0 = 9, NPROD = 64;
@@ -36,9 +37,9 @@ constexpr int THREADS = 352;
 constexpr int64_t QDIG_BLOCK = 16 * static_cast<int64_t>(B_BYTES);  // 512 KB per block
 
 struct Smem {
-  int8_t a[2][A_BYTES];
-  int8_t b[2][B_BYTES];
-  uint64_t full[2], empty[2], acc_full, acc_empty;
+  int8_t a[NST][A_BYTES];
+  int8_t b[NST][B_BYTES];
+  uint64_t full[NST], empty[NST], acc_full, acc_empty;
   uint32_t tmem;
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
@@ -65,6 +66,28 @@ __device__ __forceinline__ uint32_t slab_off(int row, int byte) {
   return static_cast<uint32_t>(row >> 3) * 1024u + sm100::sw128_offset(row & 7, byte);
 }
 
+// Y4's slab: rows of 64 B, 64-B swizzle (16-B chunk ^= (row / 2) % 4), 8-row
+// groups 512 B apart
+__device__ __forceinline__ uint32_t sw64_off(int row, int byte) {
+  return static_cast<uint32_t>(row) * 64u + ((((byte >> 4) ^ ((row >> 1) & 3)) << 4) | (byte & 15));
+}
+
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);  // start address
+  d |= static_cast<uint64_t>(1) << 16;               // LBO (unused, swizzled K-major)
+  d |= static_cast<uint64_t>(512 >> 4) << 32;        // SBO: 8 rows x 64 B
+  d |= static_cast<uint64_t>(1) << 46;               // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(4) << 61;               // SWIZZLE_64B
+  return d;
+}
+
+// A operand of y digit a at K offset ko (bytes) of the stage at ab
+__device__ __forceinline__ uint64_t a_desc(uint32_t ab, int a, uint32_t ko) {
+  return a < 4 ? sm100::desc_sw128(ab + (a >> 1) * A_SLAB + (a & 1) * 64 + ko)
+               : desc_sw64(ab + 2 * A_SLAB + ko);
+}
+
 __device__ __forceinline__ double l2d(long long v) {
   const int hi = static_cast<int>(v >> 32) + 0x43380000;
   return __hiloint2double(hi, static_cast<int>(v)) - 6755399441055744.0;
@@ -84,7 +107,7 @@ struct Ring {
   int i = 0;
   uint32_t ph = 0;
   __device__ __forceinline__ void next() {
-    if (++i == 2) {
+    if (++i == NST) {
       i = 0;
       ph ^= 1u;
     }
@@ -127,7 +150,9 @@ struct Producer {
         const int rl = 8 * g + rj[j], row = 64 * pw + rl;
         const int sig = __shfl_sync(0xffffffffu, o[g >> 2], rl & 31);
         const int c = cj[j], a = c >> 2;
-        cp_async16(base + (a >> 1) * A_SLAB + slab_off(row, (a & 1) * 64 + (c & 3) * 16),
+        const uint32_t dst = a < 4 ? base + (a >> 1) * A_SLAB + slab_off(row, (a & 1) * 64 + (c & 3) * 16)
+                                   : base + 2 * A_SLAB + sw64_off(row, (c & 3) * 16);
+        cp_async16(dst,
                    ydig + static_cast<int64_t>(sig) * (YD * P) + a * P + kb * QDIM + (c & 3) * 16,
                    row < n);
       }
@@ -165,7 +190,7 @@ __device__ __forceinline__ void mma_stage(Smem* S, uint32_t tmem, Ring& r, int k
     const uint32_t init = (kb == 0 && kk == 0) ? 0u : 1u;
     // (y digit A_, Q parity PI_, N, TMEM column): levels A_ + PI_ + 2i of one parity
 #define CI8_MMA(A_, PI_, N_, COL_, ACC_)                                                    \
-  umma_i8(tmem + (COL_), sm100::desc_sw128(ab + ((A_) >> 1) * A_SLAB + ((A_)&1) * 64 + ko), \
+  umma_i8(tmem + (COL_), a_desc(ab, (A_), ko),                                             \
           sm100::desc_sw128(bb + (PI_)*64 + ko), idesc_i8(128, (N_)), (ACC_))
     CI8_MMA(0, 0, 256, 0, init);    // levels 0 2 4 6
     CI8_MMA(0, 1, 256, 256, init);  // levels 1 3 5 7
@@ -232,7 +257,7 @@ __device__ __forceinline__ void drain_quarter(Smem* S, uint32_t lane_base, int a
 
 __device__ __forceinline__ void setup(Smem* S, int warp) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       sm100::mbar_init(&S->full[s], NPROD);  // producer arrivals + the B bulk copy's bytes
       sm100::mbar_init(&S->empty[s], 1);
     }
