@@ -514,21 +514,25 @@ __global__ void __launch_bounds__(kThreads) k_outer_f64(
 // Sparse outer products for p = 256 (config D), k <= 32 kept atoms per signal:
 // P[d][a] = sum over the segment's signals of y[d] x[a], on the CUDA cores in
 // float64 with only the kept pairs multiplied (k / p = 1/16 of the dense DMMA
-// product's work).  CTA (segment, dim quarter): 16 warps, warp w owns atoms
-// w + 16 j, lane the dims 64 q + 2 lane + {0, 1} — 32 float64 accumulators in
+// product's work).  CTA (segment, dim quarter): 32 warps, warp w owns atoms
+// w + 32 j, lane the dims 64 q + 2 lane + {0, 1} — 16 float64 accumulators in
 // registers.  Per chunk of 64 signals: the quarter's y rows as float64 and the
 // codes densified per atom in shared memory with a 64-bit signal mask per atom
 // (atomicOr: order-free); each warp walks its atoms' masks in ascending signal
 // order, so the summation order — and the partial — is deterministic.  The next
-// chunk's y and codes are prefetched into registers during the FMAs.
+// chunk's y and codes are prefetched into registers during the FMAs; the
+// partial leaves through shared memory as coalesced 2-KB rows.
 namespace osp {
-constexpr int P = 256, DQ = 64, C = 64, THREADS = 512, WARPS = 16, AW = P / WARPS;
+constexpr int P = 256, DQ = 64, C = 64, THREADS = 1024, WARPS = 32, AW = P / WARPS;
+constexpr int YPT = C * DQ / THREADS;  // y values per thread per chunk
+constexpr int TLD = P + 1;             // row stride of the transposed partial
 constexpr int KMAX = 32, CODES = C * KMAX / THREADS;  // code entries per thread
 struct Smem {
   double ys[C][DQ];
   double xval[P][C];
   uint32_t mask[2][P][C / 32];
 };
+static_assert(C * DQ + P * C >= DQ * TLD, "the transposed partial fits in ys + xval");
 }  // namespace osp
 
 template <typename TY>
@@ -545,11 +549,10 @@ __global__ void __launch_bounds__(osp::THREADS, 1) k_outer_sparse256(
   const int seg = blockIdx.x, d0 = DQ * static_cast<int>(blockIdx.y);
   const int64_t lo = seg_lo[seg], hi = seg_hi[seg];
   reinterpret_cast<uint32_t*>(S.mask)[tid] = 0u;  // both mask buffers: 2 x 256 x 2 words
-  reinterpret_cast<uint32_t*>(S.mask)[tid + THREADS] = 0u;
-  // prefetch: y row tid / 8, dims d0 + 8 (tid % 8) .. + 7; code entries e = tid + 512 i
-  // (signal e % 64, slot e / 64)
-  const int yr = tid >> 3, yc = 8 * (tid & 7);
-  double yv[8];
+  // prefetch: y row tid / 16, dims d0 + 4 (tid % 16) .. + 3; code entries
+  // e = tid + 1024 i (signal e % 64, slot e / 64)
+  const int yr = tid >> 4, yc = YPT * (tid & 15);
+  double yv[YPT];
   int ci[CODES];
   double cv[CODES];
   auto prefetch = [&](int64_t t0) {
@@ -558,10 +561,10 @@ __global__ void __launch_bounds__(osp::THREADS, 1) k_outer_sparse256(
       const int64_t r = order ? static_cast<int64_t>(order[t]) : t;
       const TY* src = y + r * P + d0 + yc;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) yv[i] = static_cast<double>(__ldg(src + i));
+      for (int i = 0; i < YPT; ++i) yv[i] = static_cast<double>(__ldg(src + i));
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) yv[i] = 0.0;
+      for (int i = 0; i < YPT; ++i) yv[i] = 0.0;
     }
 #pragma unroll
     for (int i = 0; i < CODES; ++i) {
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(osp::THREADS, 1) k_outer_sparse256(
   for (int64_t t0 = lo; t0 < hi; t0 += C) {
     // stage the prefetched chunk (the previous chunk's FMAs are done: sync below)
 #pragma unroll
-    for (int i = 0; i < 8; i += 2)
+    for (int i = 0; i < YPT; i += 2)
       *reinterpret_cast<double2*>(&S.ys[yr][yc + i]) = make_double2(yv[i], yv[i + 1]);
 #pragma unroll
     for (int i = 0; i < CODES; ++i) {
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(osp::THREADS, 1) k_outer_sparse256(
     }
     __syncthreads();
     if (t0 + C < hi) prefetch(t0 + C);
-    reinterpret_cast<uint32_t*>(S.mask[buf ^ 1])[tid] = 0u;  // the next chunk's masks
+    if (tid < P * (C / 32)) reinterpret_cast<uint32_t*>(S.mask[buf ^ 1])[tid] = 0u;  // next chunk's
 #pragma unroll
     for (int j = 0; j < AW; ++j) {
       const int a = warp + WARPS * j;
@@ -613,13 +616,17 @@ __global__ void __launch_bounds__(osp::THREADS, 1) k_outer_sparse256(
     buf ^= 1;
     __syncthreads();
   }
-  double* out = partial + static_cast<int64_t>(seg) * P * P;
+  // transpose through shared memory (ys + xval, free after the loop's last sync)
+  double* T = &S.ys[0][0];
 #pragma unroll
   for (int j = 0; j < AW; ++j) {
     const int a = warp + WARPS * j;
-    out[static_cast<int64_t>(d0 + 2 * lane) * P + a] = acc[j][0];
-    out[static_cast<int64_t>(d0 + 2 * lane + 1) * P + a] = acc[j][1];
+    T[(2 * lane) * TLD + a] = acc[j][0];
+    T[(2 * lane + 1) * TLD + a] = acc[j][1];
   }
+  __syncthreads();
+  double* out = partial + static_cast<int64_t>(seg) * P * P + static_cast<int64_t>(d0) * P;
+  for (int e = tid; e < DQ * P; e += THREADS) out[e] = T[(e / P) * TLD + e % P];
 }
 
 // P_b = sum of block b's segment partials.  A CTA owns 32 consecutive elements;
