@@ -54,36 +54,43 @@ __global__ void __launch_bounds__(256) k_ns_init(const double* __restrict__ P, i
   }
 }
 
-// C = op(A) B per matrix, 64 x 64 tile per CTA.  EPI = 1: C = c1 I + c3 (A^T B) and
-// the tile's sum of (G - I)^2 over the valid p x p region into part[b][tile].
-template <bool TRANS_A, int EPI>
-__global__ void __launch_bounds__(256) k_ns_gemm(const double* __restrict__ A,
-                                                 const double* __restrict__ B, double* C,
-                                                 int p, int PP, const int* __restrict__ done,
-                                                 double c1, double c3, double* part) {
+// C = op(A) B per matrix, TT x TT tile per CTA (TT = 64: 8 warps; TT = 32 for
+// small batches: 4 warps, four times the CTAs of one matrix).  EPI = 1:
+// C = c1 I + c3 (A^T B) and the tile's sum of (G - I)^2 over the valid p x p
+// region into part[b][tile].
+template <bool TRANS_A, int EPI, int TT>
+__global__ void __launch_bounds__(TT * 4) k_ns_gemm(const double* __restrict__ A,
+                                                   const double* __restrict__ B, double* C,
+                                                   int p, int PP, const int* __restrict__ done,
+                                                   double c1, double c3, double* part) {
+  constexpr int NT = TT * 4, NF = TT / 8;  // threads; 8-column fragments per warp
   const int b = blockIdx.y;
   if (done[b]) return;
   extern __shared__ __align__(16) unsigned char dyn[];
-  double* sA = reinterpret_cast<double*>(dyn);
-  double* sB = sA + T * LDS;
+  double* sA = reinterpret_cast<double*>(dyn);  // [i][k], stride LDS
+  double* sB = sA + T * LDS;                      // [k][j], stride LDS
   __shared__ double red[32];
-  const int nt = PP / T;
+  const int nt = PP / TT;
   const int ti = blockIdx.x / nt, tj = blockIdx.x % nt;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int64_t off = static_cast<int64_t>(b) * PP * PP;
   const double* Ab = A + off;
   const double* Bb = B + off;
-  double acc[8][2];
+  double acc[NF][2];
 #pragma unroll
-  for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
+  for (int n = 0; n < NF; ++n) acc[n][0] = acc[n][1] = 0.0;
   for (int kc = 0; kc < PP; kc += T) {
     __syncthreads();
-    for (int e = tid; e < T * T; e += 256) {
-      const int r = e >> 6, c = e & 63;
-      // sA[i][k]: output row i, reduction index k
-      if (TRANS_A) sA[c * LDS + r] = Ab[static_cast<int64_t>(kc + r) * PP + ti * T + c];
-      else sA[r * LDS + c] = Ab[static_cast<int64_t>(ti * T + r) * PP + kc + c];
-      sB[r * LDS + c] = Bb[static_cast<int64_t>(kc + r) * PP + tj * T + c];
+    for (int e = tid; e < TT * T; e += NT) {
+      if (TRANS_A) {  // op(A)[i][k] = A[k][i]
+        const int r = e / TT, c = e % TT;
+        sA[c * LDS + r] = Ab[static_cast<int64_t>(kc + r) * PP + ti * TT + c];
+      } else {
+        const int r = e >> 6, c = e & 63;
+        sA[r * LDS + c] = Ab[static_cast<int64_t>(ti * TT + r) * PP + kc + c];
+      }
+      const int rb = e / TT, cb = e % TT;
+      sB[rb * LDS + cb] = Bb[static_cast<int64_t>(kc + rb) * PP + tj * TT + cb];
     }
     __syncthreads();
     const double* ya = sA + (8 * warp + g) * LDS + t4;
@@ -92,16 +99,16 @@ __global__ void __launch_bounds__(256) k_ns_gemm(const double* __restrict__ A,
       const double a = ya[k0];
       const double* bb = sB + (k0 + t4) * LDS + g;
 #pragma unroll
-      for (int n = 0; n < 8; ++n) dmma(acc[n][0], acc[n][1], a, bb[8 * n]);
+      for (int n = 0; n < NF; ++n) dmma(acc[n][0], acc[n][1], a, bb[8 * n]);
     }
   }
-  const int row = ti * T + 8 * warp + g;
+  const int row = ti * TT + 8 * warp + g;
   double dsum = 0.0;
 #pragma unroll
-  for (int n = 0; n < 8; ++n) {
+  for (int n = 0; n < NF; ++n) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int col = tj * T + 8 * n + 2 * t4 + h;
+      const int col = tj * TT + 8 * n + 2 * t4 + h;
       double v = acc[n][h];
       if (EPI == 1) {
         const double delta = row == col ? 1.0 : 0.0;
@@ -110,11 +117,11 @@ __global__ void __launch_bounds__(256) k_ns_gemm(const double* __restrict__ A,
       }
       acc[n][h] = v;
     }
-    *reinterpret_cast<double2*>(C + off + static_cast<int64_t>(row) * PP + tj * T + 8 * n + 2 * t4) =
-        make_double2(acc[n][0], acc[n][1]);
+    *reinterpret_cast<double2*>(C + off + static_cast<int64_t>(row) * PP + tj * TT + 8 * n +
+                                2 * t4) = make_double2(acc[n][0], acc[n][1]);
   }
   if (EPI == 1) {
-    dsum = block_sum<256>(dsum, red);
+    dsum = block_sum<NT>(dsum, red);
     if (tid == 0) part[static_cast<int64_t>(b) * nt * nt + blockIdx.x] = dsum;
   }
 }
@@ -157,7 +164,7 @@ using namespace sbo;
 
 // workspace: 3 PP x PP buffers, the tile parts and 3 ints per matrix
 extern "C" size_t sbo_polar_ns_big_workspace_bytes(int K, int p) {
-  const int64_t PP = ceil_div(p, pbig::T) * pbig::T, nt = PP / pbig::T;
+  const int64_t PP = ceil_div(p, pbig::T) * pbig::T, nt = PP / 32;  // parts of 32-tiles
   return static_cast<size_t>(K) * (3 * PP * PP + nt * nt) * sizeof(double) +
          static_cast<size_t>(K) * 3 * sizeof(int) + 256;
 }
@@ -171,24 +178,28 @@ int sbo_polar_ns_big(const double* P, int K, int p, const int64_t* counts, doubl
   double* X[2] = {static_cast<double*>(ws), static_cast<double*>(ws) + K * mat};
   double* Am = X[1] + K * mat;
   double* part = Am + K * mat;
-  int* done = reinterpret_cast<int*>(part + static_cast<int64_t>(K) * nt * nt);
+  int* done = reinterpret_cast<int*>(part + static_cast<int64_t>(K) * (PP / 32) * (PP / 32));
   int* final_buf = done + K;
   int* iters = final_buf + K;
   pbig::k_ns_init<<<K, 256, 0, st>>>(P, p, PP, counts, X[0], done, final_buf, status);
-  const dim3 grid(static_cast<unsigned>(nt * nt), static_cast<unsigned>(K));
+  // small batches (the new block's rounds): 32 x 32 tiles, 4x the CTAs
+  const bool small = K <= 4;
+  const int TT = small ? 32 : pbig::T, ntt = PP / TT;
+  const dim3 grid(static_cast<unsigned>(ntt * ntt), static_cast<unsigned>(K));
   const int smem = static_cast<int>(2 * pbig::T * pbig::LDS * sizeof(double));
-  cudaFuncSetAttribute(pbig::k_ns_gemm<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(pbig::k_ns_gemm<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto g1 = small ? pbig::k_ns_gemm<true, 1, 32> : pbig::k_ns_gemm<true, 1, 64>;
+  auto g0 = small ? pbig::k_ns_gemm<false, 0, 32> : pbig::k_ns_gemm<false, 0, 64>;
+  cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(g0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   double l = 1e-6;
   int cur = 0;
   for (int it = 0; it < pbig::kMaxIter; ++it) {
     const double al = l < 0.99 ? sqrt(3.0 / (1.0 + l + l * l)) : 1.0;
     const double c1 = 1.5 * al, c3 = -0.5 * al * al * al;
-    pbig::k_ns_gemm<true, 1><<<grid, 256, smem, st>>>(X[cur], X[cur], Am, p, PP, done, c1, c3, part);
-    pbig::k_ns_check<<<(K + 127) / 128, 128, 0, st>>>(part, nt * nt, K, cur, it, done,
+    g1<<<grid, TT * 4, smem, st>>>(X[cur], X[cur], Am, p, PP, done, c1, c3, part);
+    pbig::k_ns_check<<<(K + 127) / 128, 128, 0, st>>>(part, ntt * ntt, K, cur, it, done,
                                                         final_buf, iters);
-    pbig::k_ns_gemm<false, 0><<<grid, 256, smem, st>>>(X[cur], Am, X[cur ^ 1], p, PP, done, 0.0,
-                                                     0.0, nullptr);
+    g0<<<grid, TT * 4, smem, st>>>(X[cur], Am, X[cur ^ 1], p, PP, done, 0.0, 0.0, nullptr);
     l = fmin(1.0, al * l * (3.0 - al * al * l * l) * 0.5);
     cur ^= 1;
   }
