@@ -113,3 +113,96 @@ __device__ inline RowPick pick_row(const double* Cs, int p, int k, int kind) {
 }
 
 }  // namespace sbo
+
+namespace sbo {
+
+// Per-warp shared scratch of pick_row_cand.
+struct PickScratch {
+  double v[64];
+  int16_t i[64];
+  uint32_t bm[8];
+};
+
+// pick_row for p = 256, k <= 32 with fewer instructions: the k-th largest of the
+// 32 lane maxima (a shuffle bitonic sort) bounds the k-th largest magnitude from
+// below (k distinct coefficients reach it), so the kept set lies among the
+// coefficients >= that bound — typically 20-30.  They are compacted to shared
+// memory and ranked exactly (|c| descending, index ascending: the rule of
+// pick_row_rank) in float64; more than 64 candidates fall back to pick_row.
+__device__ inline RowPick pick_row_cand(const double* Cs, int k, int kind, PickScratch& w) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  double a[8];
+  double lm = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    a[t] = fabs(Cs[lane + 32 * t]);
+    lm = fmax(lm, a[t]);
+  }
+  // descending bitonic sort of the lane maxima
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const double o = __shfl_xor_sync(full, lm, stride);
+      const bool desc = size == 32 || (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      lm = (lower == desc) ? fmax(lm, o) : fmin(lm, o);
+    }
+  }
+  const double lo = __shfl_sync(full, lm, k - 1);
+  unsigned bal[8];
+  int n = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    bal[t] = __ballot_sync(full, a[t] >= lo);
+    n += __popc(bal[t]);
+  }
+  if (n > 64) return pick_row(Cs, 256, k, kind);
+  if (lane < 8) w.bm[lane] = 0u;
+  int base = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if ((bal[t] >> lane) & 1u) {
+      const int at = base + __popc(bal[t] & lt);
+      w.v[at] = a[t];
+      w.i[at] = static_cast<int16_t>(lane + 32 * t);
+    }
+    base += __popc(bal[t]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < n) {
+      const double v = w.v[c];
+      const int id = w.i[c];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const double u = w.v[j];
+        rank += (u > v) || (u == v && w.i[j] < id);
+      }
+      if (rank < k) atomicOr(&w.bm[id >> 5], 1u << (id & 31));
+    }
+  }
+  __syncwarp();
+  RowPick r;
+  r.sel = 0u;
+  double sq = 0.0, sc = 0.0, rest = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if ((w.bm[t] >> lane) & 1u) {
+      r.sel |= 1u << t;
+      sq = fma(a[t], a[t], sq);
+      sc += a[t];
+    } else {
+      rest = fma(a[t], a[t], rest);
+    }
+  }
+  __syncwarp();  // the scratch is reused by the warp's next row
+  r.score = warp_sum(kind == SBO_KIND_SQUARED_SUM ? sq : sc);
+  r.rest_sq = warp_sum(rest);
+  return r;
+}
+
+}  // namespace sbo

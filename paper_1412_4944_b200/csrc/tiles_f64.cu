@@ -977,11 +977,13 @@ __global__ void k_select_coded(const double* __restrict__ coeffs, const int64_t*
                                int64_t t, int p, int k, int kind,
                                const int32_t* __restrict__ order, int64_t ld, int16_t* idx,
                                double* val, double* energy, double* rest_sq) {
+  __shared__ PickScratch scr[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
   if (j >= t || (n && j >= *n)) return;
   const double* Cs = coeffs + j * p;
-  const RowPick r = pick_row(Cs, p, k, kind);
+  const RowPick r = (p == 256 && k <= 32) ? pick_row_cand(Cs, k, kind, scr[warp])
+                                          : pick_row(Cs, p, k, kind);
   const int64_t col = order ? order[j] : j;
   const unsigned lt = (1u << lane) - 1u;
   int pos = 0;

@@ -224,3 +224,22 @@ def test_recheck_i8_near_tied_blocks_match_oracle(dev, kind, monkeypatch):
     n2 = (rows.astype(np.float64) ** 2).sum(1)
     assert (np.abs(s1 - s0_) <= 1e-13 * n2 + 1e-300).all()
     assert (np.abs(r1 - r0) <= 1e-13 * n2 + 1e-300).all()
+
+
+@pytest.mark.parametrize("s0", [1, 16, 32])
+def test_code_i8_exact_ties_identity_block(dev, s0):
+    """Q = I: the coefficients are the 8-bit pixel values, so nearly every signal
+    has magnitude ties at its threshold (and zero signals tie everywhere): the
+    exact rank rule (ties -> lower atom) must match oracle.top_support."""
+    rows = signals.patch_signals(4000, 16, 256, 256)
+    rows[::9] = 0.0
+    eng = _engine(dev, rows, [np.eye(P), _blocks(1, 3)[0]], s0)
+    g = eng.list_segments(eng.m)
+    n, k = eng.m, eng.k
+    idx = torch.full((k, n), -7, dtype=torch.int16, device=dev)
+    val = torch.full((k, n), np.nan, dtype=torch.float64, device=dev)
+    eng.code_i8(None, g, n, 2, 0, n, idx, val)
+    torch.cuda.synchronize()
+    oi, ov = O.top_support(rows.T.astype(np.float64), s0)
+    assert np.array_equal(idx.cpu().numpy().astype(np.int64), oi)
+    assert np.array_equal(val.cpu().numpy(), ov)
