@@ -336,6 +336,20 @@ int sbo_energy_recheck_i8(const void* ydig, int sy, const double* blocks, int K,
                           int64_t max_list, int32_t* best, double* score, double* residual,
                           void* workspace, size_t ws_bytes, void* stream);
 
+/* sbo_energy_recheck_i8 (same arguments and outputs) over (signal, candidate
+ * block) pairs: the flagged signals are bucketed per candidate block and each
+ * block's list is projected (sbo_coef_i8_segments) and ranked
+ * (sbo_select_coded) alone, so only the pairs the masks name are computed; the
+ * first maximum over each signal's candidates in ascending block order wins.
+ * list need not be sorted.  Workspace: sbo_recheck_pairs_workspace_bytes(K,
+ * max_list). */
+size_t sbo_recheck_pairs_workspace_bytes(int K, int64_t max_list);
+int sbo_energy_recheck_pairs(const void* ydig, int sy, const double* blocks, int K, int s0,
+                             int kind, const int32_t* list, const uint64_t* cand,
+                             const int32_t* nlist, int64_t max_list, int32_t* best,
+                             double* score, double* residual, void* workspace, size_t ws_bytes,
+                             void* stream);
+
 /* ---------------------------------------------------------------------------
  * Polar update Q_b = U V^T of P_b for the blocks whose count > 0 — replaces
  * linalg.py:68-78 (procrustes_polar via thin_svd/gesdd) and the guard of

@@ -62,6 +62,8 @@ _SIGS = {
     "sbo_coef_i8_workspace_bytes": (SZ, [I]),
     "sbo_coef_i8_segments": (I, [P, I, P, P, P, P, P, I64, P, I, I, P, P, SZ, P]),
     "sbo_recheck_i8_workspace_bytes": (SZ, [I]),
+    "sbo_recheck_pairs_workspace_bytes": (SZ, [I, I64]),
+    "sbo_energy_recheck_pairs": (I, [P, I, P, I, I, I, P, P, P, I64, P, P, P, P, SZ, P]),
     "sbo_energy_recheck_i8": (I, [P, I, P, I, I, I, P, P, P, I64, P, P, P, P, SZ, P]),
     "sbo_polar_workspace_bytes": (SZ, [I, I]),
     "sbo_polar": (I, [P, I, I, P, P, P, P, P, P, SZ, P]),

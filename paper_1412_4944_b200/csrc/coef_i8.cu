@@ -561,3 +561,138 @@ extern "C" int sbo_energy_recheck_i8(const void* ydig, int sy, const double* blo
       ldexp(1.0, -sy - 26), scratch, best, score, residual);
   return check_launch("k_recheck_i8");
 }
+
+// ---------------------------------------------------------------------------
+// The float64 re-decision over (signal, candidate block) pairs: the flagged
+// signals are bucketed per candidate block, each block's list is projected
+// (k_coef_i8) and ranked (sbo_select_coded) on its own — only the pairs a
+// signal's mask names are computed, where k_recheck_i8 projects every row of a
+// tile onto the union of the tile's masks — and a last pass keeps each signal's
+// first maximum over its candidate blocks in ascending order (sbo.py:191).
+// ---------------------------------------------------------------------------
+namespace sbo {
+namespace ci8 {
+
+__global__ void k_pair_lists(const int32_t* __restrict__ list, const uint64_t* __restrict__ cand,
+                             const int32_t* __restrict__ nlist, int64_t cap,
+                             unsigned long long* cnt, int32_t* pl_sig, int32_t* pl_f) {
+  const int64_t n = *nlist;
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t j = list[f];
+    for (uint64_t m = cand[f]; m; m &= m - 1) {
+      const int b = __ffsll(static_cast<long long>(m)) - 1;
+      const int64_t pos = static_cast<int64_t>(atomicAdd(cnt + b, 1ull));
+      pl_sig[b * cap + pos] = j;
+      pl_f[b * cap + pos] = static_cast<int32_t>(f);
+    }
+  }
+}
+
+__global__ void k_pair_reduce(const int32_t* __restrict__ list, const uint64_t* __restrict__ cand,
+                              const int32_t* __restrict__ nlist, int64_t cap,
+                              const double* __restrict__ s_score,
+                              const double* __restrict__ s_rest, int32_t* best, double* score,
+                              double* residual) {
+  const int64_t n = *nlist;
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double bs = -1.0, br = 0.0;
+    int bb = -1;
+    for (uint64_t m = cand[f]; m; m &= m - 1) {  // blocks ascending: first maximum wins
+      const int b = __ffsll(static_cast<long long>(m)) - 1;
+      const double sc = s_score[b * cap + f];
+      if (sc > bs) {
+        bs = sc;
+        br = s_rest[b * cap + f];
+        bb = b;
+      }
+    }
+    const int64_t j = list[f];
+    best[j] = bb;
+    score[j] = bs;
+    residual[j] = br;
+  }
+}
+
+constexpr int PAIR_CHUNK = 512;  // positions per segment of a block's pair list
+
+struct PairWs {
+  unsigned long long* cnt;
+  int64_t *seg_lo, *seg_hi;
+  int32_t *nseg, *seg_block, *pl_sig, *pl_f;
+  double *s_score, *s_rest, *coef;
+  int8_t* qdig;
+  size_t bytes;
+  int64_t max_seg;
+  PairWs(void* base, int K, int64_t cap) {
+    auto* p = static_cast<unsigned char*>(base);
+    size_t off = 0;
+    auto take = [&](size_t n) {
+      unsigned char* r = p ? p + off : nullptr;
+      off += (n + 255) & ~size_t(255);
+      return r;
+    };
+    max_seg = (cap + PAIR_CHUNK - 1) / PAIR_CHUNK;
+    if (max_seg < 1) max_seg = 1;
+    cnt = reinterpret_cast<unsigned long long*>(take(64 * 8));
+    seg_lo = reinterpret_cast<int64_t*>(take(max_seg * 8));
+    seg_hi = reinterpret_cast<int64_t*>(take(max_seg * 8));
+    nseg = reinterpret_cast<int32_t*>(take(4));
+    seg_block = reinterpret_cast<int32_t*>(take(max_seg * 4));
+    pl_sig = reinterpret_cast<int32_t*>(take(static_cast<size_t>(K) * cap * 4));
+    pl_f = reinterpret_cast<int32_t*>(take(static_cast<size_t>(K) * cap * 4));
+    s_score = reinterpret_cast<double*>(take(static_cast<size_t>(K) * cap * 8));
+    s_rest = reinterpret_cast<double*>(take(static_cast<size_t>(K) * cap * 8));
+    qdig = reinterpret_cast<int8_t*>(take(static_cast<size_t>(K) * QDIG_BLOCK));
+    coef = reinterpret_cast<double*>(take(static_cast<size_t>(cap) * P * 8));
+    bytes = off;
+  }
+};
+
+}  // namespace ci8
+}  // namespace sbo
+
+extern "C" size_t sbo_recheck_pairs_workspace_bytes(int K, int64_t max_list) {
+  return ci8::PairWs(nullptr, K, max_list > 0 ? max_list : 1).bytes;
+}
+
+extern "C" int sbo_energy_recheck_pairs(const void* ydig, int sy, const double* blocks, int K,
+                                        int s0, int kind, const int32_t* list,
+                                        const uint64_t* cand, const int32_t* nlist,
+                                        int64_t max_list, int32_t* best, double* score,
+                                        double* residual, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+  if (!ydig || !blocks || !list || !cand || !nlist || !best || !score || !residual)
+    return fail(SBO_EINVAL, "bad arguments");
+  if (K < 1 || K > 64) return fail(SBO_EINVAL, "the candidate recheck needs 1 <= K <= 64");
+  if (s0 < 1) return fail(SBO_EINVAL, "s0 must be at least 1");
+  if (max_list <= 0) return SBO_OK;
+  ci8::PairWs w(workspace, K, max_list);
+  if (!workspace || ws_bytes < w.bytes) return fail(SBO_EINVAL, "recheck_pairs workspace too small");
+  cudaStream_t st = as_stream(stream);
+  const int64_t cap = max_list;
+  SBO_CHECK_CUDA(cudaMemsetAsync(w.cnt, 0, 64 * 8, st));
+  SBO_CHECK_CUDA(cudaMemsetAsync(w.seg_block, 0, w.max_seg * 4, st));
+  const unsigned grid = static_cast<unsigned>(min64(ceil_div(cap, 256), 148 * 8));
+  ci8::k_pair_lists<<<grid, 256, 0, st>>>(list, cand, nlist, cap, w.cnt, w.pl_sig, w.pl_f);
+  if (int rc = check_launch("k_pair_lists")) return rc;
+  const size_t qbytes = static_cast<size_t>(K) * ci8::QDIG_BLOCK;
+  for (int b = 0; b < K; ++b) {
+    const int64_t* cnt_b = reinterpret_cast<const int64_t*>(w.cnt + b);
+    if (int rc = sbo_chunk_segments(cap, cnt_b, ci8::PAIR_CHUNK, w.seg_lo, w.seg_hi, w.nseg,
+                                    stream))
+      return rc;
+    if (int rc = sbo_coef_i8_segments(ydig, sy, w.pl_sig + b * cap, w.seg_block, w.seg_lo,
+                                      w.seg_hi, w.nseg, w.max_seg, blocks, K, b, w.coef, w.qdig,
+                                      qbytes, stream))
+      return rc;
+    if (int rc = sbo_select_coded(w.coef, cnt_b, cap, ci8::P, s0, kind, w.pl_f + b * cap, cap,
+                                  nullptr, nullptr, w.s_score + b * cap, w.s_rest + b * cap,
+                                  stream))
+      return rc;
+  }
+  ci8::k_pair_reduce<<<grid, 256, 0, st>>>(list, cand, nlist, cap, w.s_score, w.s_rest, best,
+                                           score, residual);
+  return check_launch("k_pair_reduce");
+}

@@ -979,8 +979,9 @@ __global__ void k_select_coded(const double* __restrict__ coeffs, const int64_t*
                                double* val, double* energy, double* rest_sq) {
   __shared__ PickScratch scr[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
-  if (j >= t || (n && j >= *n)) return;
+  const int64_t rows = n ? min64(t, *n) : t;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp; j < rows;
+       j += static_cast<int64_t>(gridDim.x) * (blockDim.x / 32)) {
   const double* Cs = coeffs + j * p;
   const RowPick r = (p == 256 && k <= 32) ? pick_row_cand(Cs, k, kind, scr[warp])
                                           : pick_row(Cs, p, k, kind);
@@ -1002,6 +1003,7 @@ __global__ void k_select_coded(const double* __restrict__ coeffs, const int64_t*
     if (energy) energy[col] = r.score;
     if (rest_sq) rest_sq[col] = r.rest_sq;
   }
+  }
 }
 
 extern "C" int sbo_select_coded(const double* coeffs, const int64_t* n, int64_t t, int p, int s0,
@@ -1012,7 +1014,9 @@ extern "C" int sbo_select_coded(const double* coeffs, const int64_t* n, int64_t 
   if (idx && !val) return fail(SBO_EINVAL, "idx without val");
   if (t <= 0) return SBO_OK;
   const int k = s0 < p ? s0 : p;
-  k_select_coded<<<static_cast<unsigned>(ceil_div(t, 8)), 256, 0, as_stream(stream)>>>(
+  // grid-stride over the rows (t may be a capacity, the count on the device)
+  k_select_coded<<<static_cast<unsigned>(min64(ceil_div(t, 8), 148 * 64)), 256, 0,
+                   as_stream(stream)>>>(
       coeffs, n, t, p, k, kind, order, ld, idx, val, energy, rest_sq);
   return check_launch("k_select_coded");
 }

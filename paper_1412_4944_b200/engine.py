@@ -416,7 +416,21 @@ class Engine:
                 self._call("sbo_cand_sort", self.flags.data_ptr(), self.cand.data_ptr(),
                            self.nflag.data_ptr(), self.m, self.flags_sorted.data_ptr(),
                            self.cand_sorted.data_ptr(), ws.data_ptr(), ws.numel(), self.stream)
-                if self.ci8:  # p = 256: the projection from the integer digits
+                if (self.ci8 and not accumulate
+                        and os.environ.get("SBO_RECHECK_PAIRS", "1") == "1"):
+                    # p = 256, full pass: per-(signal, candidate block) pairs,
+                    # projected from the integer digits block by block (the
+                    # incremental pass's masks are the incoming winner and the
+                    # appended block: its tile unions are already tight)
+                    ws = self.scratch.get("rpairs", L.size("sbo_recheck_pairs_workspace_bytes",
+                                                           b1, self.m))
+                    self._call("sbo_energy_recheck_pairs", self.ydig.data_ptr(), self.ysy,
+                               self.blocks.data_ptr(), b1, self.s0, self.kind,
+                               self.flags_sorted.data_ptr(), self.cand_sorted.data_ptr(),
+                               self.nflag.data_ptr(), self.m, s.best.data_ptr(),
+                               s.score.data_ptr(), s.residual.data_ptr(), ws.data_ptr(),
+                               ws.numel(), self.stream)
+                elif self.ci8:  # p = 256: tiles over the union of their masks
                     ws = self.scratch.get("rci8", L.size("sbo_recheck_i8_workspace_bytes", b1))
                     self._call("sbo_energy_recheck_i8", self.ydig.data_ptr(), self.ysy,
                                self.blocks.data_ptr(), b1, self.s0, self.kind,

@@ -194,9 +194,10 @@ def test_iteration_ci8_matches_dmma(dev, monkeypatch):
 def test_recheck_i8_near_tied_blocks_match_oracle(dev, kind, monkeypatch):
     """Perturbed copies of the signals' principal basis: every signal's
     energies are within the tensor-core certificate in several blocks, so most
-    signals go to the float64 re-decision (sbo_energy_recheck_i8) with
-    multi-block candidate masks.  Decisions equal the oracle's; the float64 one
-    through the DMMA recheck gives the same state."""
+    signals go to the float64 re-decision with multi-block candidate masks.
+    Decisions equal the oracle's through the pair lists
+    (sbo_energy_recheck_pairs), the tile unions (sbo_energy_recheck_i8) and the
+    DMMA recheck; the two digit rechecks agree bit for bit."""
     rows = signals.patch_signals(3000, 16, 512, 512)
     # only near-copies compete
     base = np.linalg.eigh(rows.T.astype(np.float64) @ rows.astype(np.float64))[1][:, ::-1]
@@ -206,8 +207,9 @@ def test_recheck_i8_near_tied_blocks_match_oracle(dev, kind, monkeypatch):
         q, r = np.linalg.qr(base + 2e-8 * (i + 1) * rng.standard_normal((P, P)))
         qs.append(q * np.sign(np.diag(r)))
     states = []
-    for flag in ("1", "0"):
+    for flag, pairs in (("1", "1"), ("1", "0"), ("0", "1")):
         monkeypatch.setenv("SBO_CI8", flag)
+        monkeypatch.setenv("SBO_RECHECK_PAIRS", pairs)
         eng = Engine(Signals.from_rows(rows, dev), 16, kind, k_cap=len(qs))
         eng.set_blocks(np.stack(qs))
         assert eng.ci8 == (flag == "1")
@@ -218,9 +220,11 @@ def test_recheck_i8_near_tied_blocks_match_oracle(dev, kind, monkeypatch):
         states.append((st.best.cpu().numpy(), st.score.cpu().numpy(),
                        st.residual.cpu().numpy()))
     r = O.code_signals(rows.T.astype(np.float64), qs, 16, kind)
-    (b1, s1, r1), (b0, s0_, r0) = states
+    (bp, sp, rp), (b1, s1, r1), (b0, s0_, r0) = states  # pairs, tile unions, DMMA
+    np.testing.assert_array_equal(bp, r.block)
     np.testing.assert_array_equal(b1, r.block)
     np.testing.assert_array_equal(b0, r.block)
+    assert np.array_equal(sp, s1) and np.array_equal(rp, r1)  # same digits, same selection
     n2 = (rows.astype(np.float64) ** 2).sum(1)
     assert (np.abs(s1 - s0_) <= 1e-13 * n2 + 1e-300).all()
     assert (np.abs(r1 - r0) <= 1e-13 * n2 + 1e-300).all()
