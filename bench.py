@@ -196,6 +196,17 @@ def kernel_families(timer, p, k):
            "sbo_code_segments": ("k_code_f64", 2 * p * p, 2 * p * p, "fp64 CUDA cores"),
            "sbo_residual_segments": ("k_round64<resid>", 2 * p * p, 2 * p * p,
                                      "fp64 tensor cores (DMMA)"),
+           "sbo_tc_energy256": ("k_energy_tc256", 2 * p * p, 6 * p * p, "tcgen05 split-fp16"),
+           # p = 256: 7680 digit-product columns x 256 atoms x 2 int8 ops per signal
+           # (coef_i8.cu: 16 stages x 2 k-steps x 1920 columns x 32 deep x 2 / 256)
+           "sbo_coef_i8_segments": ("k_coef_i8", 2 * p * p, 2 * 256 * 7680,
+                                    "tcgen05 kind::i8 (exact integer digits)"),
+           "sbo_select_coded": ("k_select_coded", 0, 0, "fp64 CUDA cores, selection"),
+           # p = 256: the kept pairs only (k_outer_sparse256); p <= 64: dense DMMA
+           "sbo_outer_segments": ("k_outer_sparse256" if p == 256 else "k_outer_f64",
+                                  2 * p * k, 2 * p * k if p == 256 else 2 * p * p,
+                                  "fp64 CUDA cores (kept pairs)" if p == 256
+                                  else "fp64 tensor cores (DMMA)"),
            "sbo_polar": ("k_polar_ns_cluster", 0, 0, "fp64 tensor cores (DMMA), latency"),
            "sbo_energy_recheck": ("k_energy_f64 recheck", 0, 0, "fp64 tensor cores (DMMA)"),
            "sbo_energy_recheck_cand": ("k_energy_f64 recheck (candidates)", 0, 0,
@@ -359,7 +370,20 @@ KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2,
                     "sbo_round_code_segments": 1, "sbo_outer_i8_segments": 1, "sbo_i8_scan": 1,
                     "sbo_y_digits": 1, "sbo_y_tiles": 1, "sbo_round_i8_segments": 2,
-                    "sbo_gram_counted": 3, "sbo_chunk_segments": 1}
+                    "sbo_gram_counted": 3, "sbo_chunk_segments": 1,
+                    "sbo_tc_split_signals": 1, "sbo_tc_split_blocks": 1, "sbo_tc_energy": 1,
+                    "sbo_tc_energy256": 1, "sbo_energy_recheck_cand": 1,
+                    "sbo_coef_i8_segments": 2, "sbo_select_coded": 1,
+                    "sbo_energy_recheck_i8": 2}
+
+
+def kernels_per_call(name: str, p: int, K: int) -> int:
+    """Kernel launches behind one ABI call (gpu_launches)."""
+    if name == "sbo_polar" and p > 64:
+        return 3 + 3 * 40  # init, 40 x (2 GEMMs + check), finish, the Jacobi fallback
+    if name == "sbo_energy_recheck_pairs":
+        return 2 + 4 * K   # lists, reduce; per block: segments, digits, projection, selection
+    return KERNELS_PER_CALL.get(name, 1)
 
 
 def max_over_ranks(x: float, dist, dev) -> float:
@@ -494,7 +518,7 @@ def run_ours(a):
     elapsed = max_over_ranks(elapsed, dist if world > 1 else None, dev)
     t_step = elapsed / a.steps
     value = m_total / t_step
-    launches = a.steps * sum(KERNELS_PER_CALL.get(n, 1) * c for n, c in calls.items())
+    launches = a.steps * sum(kernels_per_call(n, p, a.K) * c for n, c in calls.items())
     hbm, bf16, src = peaks()
     kernels = kernel_families(eng.timer, p, min(a.s0, p))
     eng.timer = None

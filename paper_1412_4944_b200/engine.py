@@ -601,7 +601,7 @@ class Engine:
                 self._call("sbo_outer_segments", self.sig.y.data_ptr(), self.sig.code, p,
                            _ptr(order), g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
                            g.nseg.data_ptr(), g.max_seg, self.s0, ld, idx.data_ptr(),
-                           val.data_ptr(), partial.data_ptr(), self.stream)
+                           val.data_ptr(), partial.data_ptr(), self.stream, units=n)
             if self.i8 is None:
                 self._call("sbo_reduce_segments", partial.data_ptr(),
                            None if single else g.seg_block.data_ptr(), g.nseg.data_ptr(),
