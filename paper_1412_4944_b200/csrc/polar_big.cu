@@ -9,6 +9,7 @@
 // to a multiple of 64 with zeros, which the iteration keeps at zero.  Matrices that
 // do not converge go to the one-sided Jacobi kernel, as for p = 64.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -191,7 +192,13 @@ int sbo_polar_ns_big(const double* P, int K, int p, const int64_t* counts, doubl
   auto g0 = small ? pbig::k_ns_gemm<false, 0, 32> : pbig::k_ns_gemm<false, 0, 64>;
   cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(g0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  double l = 1e-6;
+  // lower bound of sigma_min / ||P||_F for the scaling (a ratio below it only costs
+  // iterations, never accuracy: the stop test is on ||X^T X - I||)
+  static const double l0 = [] {
+    const char* e = std::getenv("SBO_NS_L0_BIG");
+    return e ? std::atof(e) : 1e-6;
+  }();
+  double l = l0;
   int cur = 0;
   for (int it = 0; it < pbig::kMaxIter; ++it) {
     const double al = l < 0.99 ? sqrt(3.0 / (1.0 + l + l * l)) : 1.0;
