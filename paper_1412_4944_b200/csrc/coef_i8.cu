@@ -576,16 +576,37 @@ namespace ci8 {
 __global__ void k_pair_lists(const int32_t* __restrict__ list, const uint64_t* __restrict__ cand,
                              const int32_t* __restrict__ nlist, int64_t cap,
                              unsigned long long* cnt, int32_t* pl_sig, int32_t* pl_f) {
+  // per CTA: a shared histogram of the tile's pairs per block, one global
+  // reservation per (CTA, block), then the scatter (positions within a block's
+  // list are unordered: each pair's result does not depend on them)
+  __shared__ unsigned long long base[64];
+  __shared__ unsigned int hist[64];
   const int64_t n = *nlist;
-  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < n;
-       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t j = list[f];
-    for (uint64_t m = cand[f]; m; m &= m - 1) {
-      const int b = __ffsll(static_cast<long long>(m)) - 1;
-      const int64_t pos = static_cast<int64_t>(atomicAdd(cnt + b, 1ull));
-      pl_sig[b * cap + pos] = j;
-      pl_f[b * cap + pos] = static_cast<int32_t>(f);
+  for (int64_t f0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; f0 < n;
+       f0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (threadIdx.x < 64) hist[threadIdx.x] = 0u;
+    __syncthreads();
+    const int64_t f = f0 + threadIdx.x;
+    const uint64_t mask = f < n ? cand[f] : 0ull;
+    for (uint64_t m = mask; m; m &= m - 1) atomicAdd(&hist[__ffsll(static_cast<long long>(m)) - 1], 1u);
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      base[threadIdx.x] = hist[threadIdx.x] ? atomicAdd(cnt + threadIdx.x,
+                                                        static_cast<unsigned long long>(hist[threadIdx.x]))
+                                            : 0ull;
+      hist[threadIdx.x] = 0u;
     }
+    __syncthreads();
+    if (f < n) {
+      const int32_t j = list[f];
+      for (uint64_t m = mask; m; m &= m - 1) {
+        const int b = __ffsll(static_cast<long long>(m)) - 1;
+        const int64_t pos = static_cast<int64_t>(base[b] + atomicAdd(&hist[b], 1u));
+        pl_sig[b * cap + pos] = j;
+        pl_f[b * cap + pos] = static_cast<int32_t>(f);
+      }
+    }
+    __syncthreads();
   }
 }
 
