@@ -219,7 +219,7 @@ int sbo_round_i8_segments(const void* ydig, int sy, const int32_t* order,
                           void* stream);
 
 /* Sparse outer products P = Y X^T per block on the tcgen05 tensor cores
- * (onb.py:127-134; north_star "grouped GEMM Y_j X_j^T"), p = 64, float32
+ * (onb.py:127-134; north_star "grouped GEMM Y_j X_j^T"), p = 64 or 256, float32
  * signals: y (as the transposed digit tiles of sbo_y_tiles, built once per
  * grouping) and the code values cut into
  * 7-bit integer digits (y = Y_int 2^-sy exactly, 5 digits; x rounded to the
@@ -231,8 +231,9 @@ int sbo_round_i8_segments(const void* ydig, int sy, const int32_t* order,
  * the result sbo_reduce_segments would give.  Codes are read at column t of
  * the segment order (sbo_round_code_segments).  sy / sx come from sbo_i8_scan:
  * every |y| < 2^(35 - sy) on the 2^-sy grid, every |x| < 2^(54 - sx).
- * Workspace: sbo_outer_i8_workspace_bytes(nblocks). */
-size_t sbo_outer_i8_workspace_bytes(int nblocks);
+ * p = 256 runs the p = 64 product on each of the 16 (64-dim, 64-atom) slices.
+ * Workspace: sbo_outer_i8_workspace_bytes(nblocks, p). */
+size_t sbo_outer_i8_workspace_bytes(int nblocks, int p);
 int sbo_outer_i8_segments(const void* ytiles, int p, const int32_t* seg_block,
                           const int64_t* seg_lo,
                           const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
@@ -243,9 +244,10 @@ int sbo_outer_i8_segments(const void* ytiles, int p, const int32_t* seg_block,
 /* Transposed digit tiles of a segment table for sbo_outer_i8_segments: per
  * (segment, 128-position chunk) in segment order, the 5 digit planes of the
  * signals order[t] as [64 dims][128 signals] int8 (40 KB, the kernel's shared
- * memory image).  tiles: sbo_y_tiles_bytes(n, max_seg) bytes (n = positions). */
-size_t sbo_y_tiles_bytes(int64_t n, int64_t max_seg);
-int sbo_y_tiles(const void* ydig, const int32_t* order, const int64_t* seg_lo,
+ * memory image; p = 256: four such images per chunk, one per 64-dim group).
+ * tiles: sbo_y_tiles_bytes(n, max_seg, p) bytes (n = positions). */
+size_t sbo_y_tiles_bytes(int64_t n, int64_t max_seg, int p);
+int sbo_y_tiles(const void* ydig, int p, const int32_t* order, const int64_t* seg_lo,
                 const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg, void* tiles,
                 void* stream);
 

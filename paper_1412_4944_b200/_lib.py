@@ -48,9 +48,9 @@ _SIGS = {
     "sbo_round_i8_workspace_bytes": (SZ, [I]),
     "sbo_round_i8_segments": (I, [P, I, P, P, P, P, P, I64, P, I, I, I, I, I, I64, P, P, P, P,
                                   P, SZ, P]),
-    "sbo_y_tiles_bytes": (SZ, [I64, I64]),
-    "sbo_y_tiles": (I, [P, P, P, P, P, I64, P, P]),
-    "sbo_outer_i8_workspace_bytes": (SZ, [I]),
+    "sbo_y_tiles_bytes": (SZ, [I64, I64, I]),
+    "sbo_y_tiles": (I, [P, I, P, P, P, P, I64, P, P]),
+    "sbo_outer_i8_workspace_bytes": (SZ, [I, I]),
     "sbo_i8_scan": (I, [P, I, I64, I, P, P]),
     "sbo_y_digits": (I, [P, I, I64, I, I, P, P]),
     "sbo_gram_workspace_bytes": (SZ, [I64, I, I]),

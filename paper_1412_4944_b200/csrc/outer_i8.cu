@@ -62,10 +62,14 @@ struct Smem {
   int base;
 };
 
-// the CTA's contiguous range of segments
-__device__ __forceinline__ void seg_range(int nseg, int& s0, int& s1) {
-  s0 = static_cast<int>(static_cast<int64_t>(nseg) * blockIdx.x / gridDim.x);
-  s1 = static_cast<int>(static_cast<int64_t>(nseg) * (blockIdx.x + 1) / gridDim.x);
+// the CTA's contiguous range of segments: range r of nr (default: the CTA index)
+__device__ __forceinline__ void seg_range(int nseg, int& s0, int& s1, int r = -1, int nr = 0) {
+  if (r < 0) {
+    r = static_cast<int>(blockIdx.x);
+    nr = static_cast<int>(gridDim.x);
+  }
+  s0 = static_cast<int>(static_cast<int64_t>(nseg) * r / nr);
+  s1 = static_cast<int>(static_cast<int64_t>(nseg) * (r + 1) / nr);
 }
 
 // tile slot of segment s0's first tile: tiles of the segments before it (each
@@ -129,6 +133,11 @@ struct Ring {
   }
 };
 
+// PD = 256 (config D): CTA (range, combo = blockIdx.x % 16): atom group ag = combo / 4 and
+// dim group dg = combo % 4 of 64 each — the p = 64 product on the 64 x 64 slice,
+// the Y tile of the dim group (a 40-KB image of its own) and the X planes of the
+// atom group's kept pairs.
+template <int PD>
 __global__ void __launch_bounds__(THREADS, 1)
 k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_block,
            const int64_t* __restrict__ seg_lo,
@@ -153,8 +162,14 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = S->tmem;
+  // PD = 256: the 16 slices of one segment range are consecutive CTAs, so they
+  // run together and share the range's Y tiles and codes in L2
+  constexpr int NG = PD / P;  // 64-wide groups per dimension
+  const int combo = static_cast<int>(blockIdx.x) % (NG * NG);
+  const int ag = combo / NG, dg = combo % NG;
   int sa, sb;
-  seg_range(nseg, sa, sb);
+  seg_range(nseg, sa, sb, static_cast<int>(blockIdx.x) / (NG * NG),
+            static_cast<int>(gridDim.x) / (NG * NG));
   const int slot0 = tile_base(seg_lo, seg_hi, sa, &S->base);
 
   if (warp >= 4) {  // ------------------------------------------------ producers
@@ -188,8 +203,8 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
         sm100::mbar_wait(&S->empty[r.i], r.ph ^ 1u);
         if (pt == 0) {
           sm100::mbar_expect_tx(&S->fully[r.i], YTILE);
-          sm100::bulk_g2s(S->y[r.i], ytiles + static_cast<int64_t>(slot) * YTILE, YTILE,
-                          &S->fully[r.i]);
+          sm100::bulk_g2s(S->y[r.i], ytiles + (static_cast<int64_t>(slot) * NG + dg) * YTILE,
+                          YTILE, &S->fully[r.i]);
         }
         int8_t* xs = S->x[r.i];
         {
@@ -198,6 +213,8 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
         }
         asm volatile("bar.sync 2, %0;" ::"r"(NPROD));  // X planes zeroed
         auto put = [&](int j, double x, int sl) {
+          j -= P * ag;  // the atom group's slice
+          if (NG > 1 && (j < 0 || j >= P)) return;
           const long long v = __double2ll_rn(x * xscale);
           const uint32_t off = plane_off(j, sl);
           xs[xslot(0) * PLANE + off] = static_cast<int8_t>(v >> 49);
@@ -290,7 +307,8 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
         const int j = e & 63;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * warp) << 16);
         // block accumulators: [blk][0: levels 0-3 | 1: levels 4-7][dim][atom]
-        unsigned long long* out = acc64 + static_cast<int64_t>(blk) * 2 * P * P;
+        unsigned long long* out = acc64 + static_cast<int64_t>(blk) * 2 * PD * PD +
+                                  static_cast<int64_t>(P * dg) * PD + P * ag;
         for (int d0 = 0; d0 < P; d0 += EPI_DIMS) {
           uint32_t v[8][EPI_DIMS];  // [slot][dim]: top slots = levels 0..7, bottom = 4..7
 #pragma unroll
@@ -310,8 +328,8 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
             long long lo = 0;
 #pragma unroll
             for (int L = 4; L < 8; ++L) lo = lo * 128 + static_cast<int>(v[L][q]);
-            unsigned long long* o = out + (d0 + q) * P + j;
-            atomicAdd(o + P * P, static_cast<unsigned long long>(lo));
+            unsigned long long* o = out + (d0 + q) * PD + j;
+            atomicAdd(o + PD * PD, static_cast<unsigned long long>(lo));
             if (top) {
               long long hi = 0;
 #pragma unroll
@@ -339,6 +357,8 @@ k_outer_i8(const int8_t* __restrict__ ytiles, const int32_t* __restrict__ seg_bl
 // byte block transposed with PRMT.
 constexpr int YT_THREADS = 256;
 
+// PD = 256: per tile, four consecutive 40-KB images, one per 64-dim group.
+template <int PD>
 __global__ void __launch_bounds__(YT_THREADS)
 k_y_tiles(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
           const int64_t* __restrict__ seg_lo, const int64_t* __restrict__ seg_hi,
@@ -358,6 +378,7 @@ k_y_tiles(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
       if (tid < TS) srow[tid] = tid < n ? (order ? static_cast<int64_t>(order[t0 + tid]) : t0 + tid)
                                         : -1;
       __syncthreads();
+      for (int dg = 0; dg < PD / P; ++dg) {
       for (int it = tid; it < (TS / 4) * (P / 4); it += YT_THREADS) {
         const int w = it & 15, q = it >> 4;
         uint32_t wv[YD][4];
@@ -365,9 +386,10 @@ k_y_tiles(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         for (int u = 0; u < 4; ++u) {
           const int sl = 4 * q + u;
           const uint32_t* src =
-              reinterpret_cast<const uint32_t*>(ydig + (sl < n ? srow[sl] : 0) * (YD * P)) + w;
+              reinterpret_cast<const uint32_t*>(ydig + (sl < n ? srow[sl] : 0) * (YD * PD) +
+                                                P * dg) + w;
 #pragma unroll
-          for (int a = 0; a < YD; ++a) wv[a][u] = sl < n ? __ldg(src + a * (P / 4)) : 0u;
+          for (int a = 0; a < YD; ++a) wv[a][u] = sl < n ? __ldg(src + a * (PD / 4)) : 0u;
         }
 #pragma unroll
         for (int a = 0; a < YD; ++a) {
@@ -383,22 +405,25 @@ k_y_tiles(const int8_t* __restrict__ ydig, const int32_t* __restrict__ order,
         }
       }
       __syncthreads();
-      uint4* dst = reinterpret_cast<uint4*>(tiles + static_cast<int64_t>(slot) * YTILE);
+      uint4* dst = reinterpret_cast<uint4*>(
+          tiles + (static_cast<int64_t>(slot) * (PD / P) + dg) * YTILE);
       const uint4* srcs = reinterpret_cast<const uint4*>(st);
       for (int e = tid; e < static_cast<int>(YTILE / 16); e += YT_THREADS) dst[e] = srcs[e];
       __syncthreads();
+      }
     }
   }
 }
 
 // P[b][i][j] = 2^(77-sy-sx) (HI 128^-3 + LO 128^-7) from the int64 accumulators
+template <int PD>
 __global__ void k_i8_finalize(const unsigned long long* __restrict__ acc64, int nblocks,
                               double pscale, double* __restrict__ Pout) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= static_cast<int64_t>(nblocks) * P * P) return;
-  const int64_t b = e / (P * P), ij = e % (P * P);
-  const long long hi = static_cast<long long>(acc64[(2 * b) * P * P + ij]);
-  const long long lo = static_cast<long long>(acc64[(2 * b + 1) * P * P + ij]);
+  if (e >= static_cast<int64_t>(nblocks) * PD * PD) return;
+  const int64_t b = e / (PD * PD), ij = e % (PD * PD);
+  const long long hi = static_cast<long long>(acc64[(2 * b) * PD * PD + ij]);
+  const long long lo = static_cast<long long>(acc64[(2 * b + 1) * PD * PD + ij]);
   Pout[e] = fma(static_cast<double>(hi), 4.76837158203125e-07,
                 static_cast<double>(lo) * 1.7763568394002505e-15) * pscale;
 }
@@ -507,27 +532,29 @@ extern "C" int sbo_y_digits(const void* y, int dtype, int64_t m, int p, int sy, 
   return check_launch("k_y_digits");
 }
 
-extern "C" size_t sbo_y_tiles_bytes(int64_t n, int64_t max_seg) {
+extern "C" size_t sbo_y_tiles_bytes(int64_t n, int64_t max_seg, int p) {
   return static_cast<size_t>(ceil_div(n > 0 ? n : 0, oi8::TS) + (max_seg > 0 ? max_seg : 0)) *
-         oi8::YTILE;
+         oi8::YTILE * (p == 256 ? 4 : 1);
 }
 
-extern "C" int sbo_y_tiles(const void* ydig, const int32_t* order, const int64_t* seg_lo,
+extern "C" int sbo_y_tiles(const void* ydig, int p, const int32_t* order, const int64_t* seg_lo,
                            const int64_t* seg_hi, const int32_t* nseg, int64_t max_seg,
                            void* tiles, void* stream) {
   if (!ydig || !tiles) return fail(SBO_EINVAL, "bad arguments");
+  if (p != 64 && p != 256) return fail(SBO_EINVAL, "digit tiles need p = 64 or 256");
   if (max_seg <= 0) return SBO_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = static_cast<unsigned>(min64(max_seg, 4 * sms));
-  oi8::k_y_tiles<<<grid, oi8::YT_THREADS, 0, as_stream(stream)>>>(
+  auto kern = p == 256 ? oi8::k_y_tiles<256> : oi8::k_y_tiles<64>;
+  kern<<<grid, oi8::YT_THREADS, 0, as_stream(stream)>>>(
       static_cast<const int8_t*>(ydig), order, seg_lo, seg_hi, nseg, static_cast<int8_t*>(tiles));
   return check_launch("k_y_tiles");
 }
 
-extern "C" size_t sbo_outer_i8_workspace_bytes(int nblocks) {
-  return static_cast<size_t>(nblocks > 0 ? nblocks : 0) * 2 * 64 * 64 * sizeof(long long);
+extern "C" size_t sbo_outer_i8_workspace_bytes(int nblocks, int p) {
+  return static_cast<size_t>(nblocks > 0 ? nblocks : 0) * 2 * p * p * sizeof(long long);
 }
 
 extern "C" int sbo_outer_i8_segments(const void* ytiles, int p, const int32_t* seg_block,
@@ -537,33 +564,34 @@ extern "C" int sbo_outer_i8_segments(const void* ytiles, int p, const int32_t* s
                                      const int16_t* idx, const double* val, int sy, int sx,
                                      double* P, void* workspace, size_t ws_bytes,
                                      void* stream) {
-  if (p != 64) return fail(SBO_EINVAL, "the tensor-core outer product needs p = 64");
+  if (p != 64 && p != 256) return fail(SBO_EINVAL, "the tensor-core outer product needs p = 64 or 256");
   if (s0 < 1 || !idx || !val || !P || nblocks < 1) return fail(SBO_EINVAL, "bad arguments");
-  if (ws_bytes < sbo_outer_i8_workspace_bytes(nblocks) || !workspace)
+  if (ws_bytes < sbo_outer_i8_workspace_bytes(nblocks, p) || !workspace)
     return fail(SBO_EINVAL, "outer_i8 workspace too small");
   const int k = s0 < p ? s0 : p;
   cudaStream_t st = as_stream(stream);
-  SBO_CHECK_CUDA(cudaMemsetAsync(workspace, 0, sbo_outer_i8_workspace_bytes(nblocks), st));
+  SBO_CHECK_CUDA(cudaMemsetAsync(workspace, 0, sbo_outer_i8_workspace_bytes(nblocks, p), st));
   auto* acc = static_cast<unsigned long long*>(workspace);
   if (max_seg > 0) {
-    static bool attr = false;
-    if (!attr) {
-      SBO_CHECK_CUDA(cudaFuncSetAttribute(oi8::k_outer_i8,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = p == 256 ? oi8::k_outer_i8<256> : oi8::k_outer_i8<64>;
+    static bool attr[2] = {false, false};
+    if (!attr[p == 256]) {
+      SBO_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(oi8::SMEM_BYTES)));
-      attr = true;
+      attr[p == 256] = true;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = static_cast<unsigned>(min64(max_seg, sms));
-    oi8::k_outer_i8<<<grid, oi8::THREADS, oi8::SMEM_BYTES, st>>>(
+    const unsigned grid = static_cast<unsigned>(min64(max_seg, sms)) * (p == 256 ? 16u : 1u);
+    kern<<<grid, oi8::THREADS, oi8::SMEM_BYTES, st>>>(
         static_cast<const int8_t*>(ytiles), seg_block, seg_lo, seg_hi, nseg, k, ld, idx,
         val, ldexp(1.0, sx), acc);
     if (int rc = check_launch("k_outer_i8")) return rc;
   }
-  const int64_t n = static_cast<int64_t>(nblocks) * 64 * 64;
-  oi8::k_i8_finalize<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, st>>>(
-      acc, nblocks, ldexp(1.0, 77 - sy - sx), P);
+  const int64_t n = static_cast<int64_t>(nblocks) * p * p;
+  auto fin = p == 256 ? oi8::k_i8_finalize<256> : oi8::k_i8_finalize<64>;
+  fin<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, st>>>(acc, nblocks,
+                                                               ldexp(1.0, 77 - sy - sx), P);
   return check_launch("k_i8_finalize");
 }

@@ -279,19 +279,21 @@ class Engine:
         if lsb + sy < 0 or sy > 126 + 35:
             return  # some value is finer than the 35-bit grid: not exact
         self.ysy = sy
+        xmax = math.sqrt(norm2) * (1.0 + 1e-6)  # |x| <= ||y|| (orthonormal blocks)
+        ex = math.floor(math.log2(xmax)) + 1 if xmax > 0 else 0
         if self.p == 256:
-            # p = 256: the rounds' projection from the digits (coef_i8.cu); the
-            # outer product stays float64
+            # p = 256: the rounds' projection from the digits (coef_i8.cu) and the
+            # outer product on the 16 (64-dim, 64-atom) slices (outer_i8.cu)
             self.ci8 = os.environ.get("SBO_CI8", "1") == "1"
             if self.ci8:
+                if self.k <= 32 and os.environ.get("SBO_OI8_256", "1") == "1":
+                    self.i8 = (sy, 54 - ex)
                 self.ydig = torch.empty((self.m, 5 * 256), dtype=torch.int8, device=self.dev)
                 self._call("sbo_y_digits", self.sig.y.data_ptr(), self.sig.code, self.m,
                            self.p, sy, self.ydig.data_ptr(), self.stream)
             else:
                 self.ysy = None
             return
-        xmax = math.sqrt(norm2) * (1.0 + 1e-6)  # |x| <= ||y|| (orthonormal blocks)
-        ex = math.floor(math.log2(xmax)) + 1 if xmax > 0 else 0
         self.i8 = (sy, 54 - ex)
         # the round's projection from the same digits (k <= 32 selection networks)
         self.ri8 = self.k <= 32 and os.environ.get("SBO_RI8", "1") == "1"
@@ -545,11 +547,11 @@ class Engine:
                    else None)
         i8_ws = ytiles = None
         if self.i8 is not None:
-            i8_ws = self.scratch.get("i8", L.size("sbo_outer_i8_workspace_bytes", nblocks))
+            i8_ws = self.scratch.get("i8", L.size("sbo_outer_i8_workspace_bytes", nblocks, p))
             # transposed digit tiles of this grouping, shared by its R rounds
             ytiles = self.scratch.get("ytiles_list" if single else "ytiles",
-                                      L.size("sbo_y_tiles_bytes", n, g.max_seg))
-            self._call("sbo_y_tiles", self.ydig.data_ptr(), _ptr(order), g.seg_lo.data_ptr(),
+                                      L.size("sbo_y_tiles_bytes", n, g.max_seg, p))
+            self._call("sbo_y_tiles", self.ydig.data_ptr(), p, _ptr(order), g.seg_lo.data_ptr(),
                        g.seg_hi.data_ptr(), g.nseg.data_ptr(), g.max_seg, ytiles.data_ptr(),
                        self.stream, units=n)
         P = self.scratch.get("P", 8 * nblocks * p * p)
@@ -574,6 +576,9 @@ class Engine:
                                self.blocks.data_ptr(), nb, override, self.s0, 0, self.kind,
                                ld, idx.data_ptr(), val.data_ptr(), None, None, ws.data_ptr(),
                                ws.numel(), self.stream, units=n)
+                elif self.ci8:  # p = 256
+                    self.code_i8(order, g, n, nblocks, first_block if single else -1, ld,
+                                 idx, val, count=g.count)
                 else:
                     self._call("sbo_round_code_segments", self.sig.y.data_ptr(),
                                self.sig.code, p, _ptr(order), g.seg_block.data_ptr(),

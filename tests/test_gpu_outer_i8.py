@@ -42,12 +42,12 @@ def _p_i8_and_f64(eng, g, n, order, nblocks, idx, val, seg_block):
     order_p = order.data_ptr() if order is not None else None
     P_i8 = torch.zeros((nblocks, 64, 64), dtype=torch.float64, device=eng.dev)
     P_f64 = torch.zeros_like(P_i8)
-    ws = torch.empty(L.size("sbo_outer_i8_workspace_bytes", nblocks), dtype=torch.uint8,
+    ws = torch.empty(L.size("sbo_outer_i8_workspace_bytes", nblocks, 64), dtype=torch.uint8,
                      device=eng.dev)
     sy, sx = eng.i8
-    tiles = torch.empty(L.size("sbo_y_tiles_bytes", n, g.max_seg), dtype=torch.uint8,
+    tiles = torch.empty(L.size("sbo_y_tiles_bytes", n, g.max_seg, 64), dtype=torch.uint8,
                         device=eng.dev)
-    L.call("sbo_y_tiles", eng.ydig.data_ptr(), order_p, g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
+    L.call("sbo_y_tiles", eng.ydig.data_ptr(), 64, order_p, g.seg_lo.data_ptr(), g.seg_hi.data_ptr(),
            g.nseg.data_ptr(), g.max_seg, tiles.data_ptr(), st)
     L.call("sbo_outer_i8_segments", tiles.data_ptr(), 64,
            seg_block.data_ptr() if seg_block is not None else None, g.seg_lo.data_ptr(),
