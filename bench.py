@@ -190,8 +190,9 @@ def kernel_families(timer, p, k):
            # 1920 digit-product columns x 64 dims x 2 int8 ops per signal (round_i8.cu)
            "sbo_round_i8_segments": ("k_round_i8", 2 * p * p, 2 * 64 * 1920,
                                      "tcgen05 kind::i8 (exact integer digits)"),
-           # 1280 digit-product columns x 128 rows x 2 int8 ops per signal (outer_i8.cu)
-           "sbo_outer_i8_segments": ("k_outer_i8", 2 * p * k, 2 * 128 * 1280,
+           # 1280 digit-product columns x 128 rows x 2 int8 ops per signal and 64 x 64
+           # slice (outer_i8.cu; p = 256: 16 slices)
+           "sbo_outer_i8_segments": ("k_outer_i8", 2 * p * k, 2 * 128 * 1280 * (p // 64) ** 2,
                                      "tcgen05 kind::i8 (exact integer digits)"),
            "sbo_code_segments": ("k_code_f64", 2 * p * p, 2 * p * p, "fp64 CUDA cores"),
            "sbo_residual_segments": ("k_round64<resid>", 2 * p * p, 2 * p * p,
@@ -368,7 +369,7 @@ KERNELS_PER_CALL = {"sbo_energy_pass": 1, "sbo_group": 4, "sbo_code_segments": 1
                     "sbo_outer_segments": 1, "sbo_reduce_segments": 1, "sbo_polar": 2,
                     "sbo_gram": 3, "sbo_init_block": 1, "sbo_worst_set": 19, "sbo_sum": 2,
                     "sbo_key_histogram": 1, "sbo_worst_collect": 3, "sbo_frobenius_sq": 2,
-                    "sbo_round_code_segments": 1, "sbo_outer_i8_segments": 1, "sbo_i8_scan": 1,
+                    "sbo_round_code_segments": 1, "sbo_outer_i8_segments": 2, "sbo_i8_scan": 1,
                     "sbo_y_digits": 1, "sbo_y_tiles": 1, "sbo_round_i8_segments": 2,
                     "sbo_gram_counted": 3, "sbo_chunk_segments": 1,
                     "sbo_tc_split_signals": 1, "sbo_tc_split_blocks": 1, "sbo_tc_energy": 1,
