@@ -11,3 +11,7 @@ timeout 900 ncu --nvtx --nvtx-include "iteration/" --metrics gpu__time_duration.
    --log-file gpurun_out/launches.csv python tools/profile_iteration.py > gpurun_out/launches.log 2>&1
 python tools/launch_summary.py gpurun_out/launches.csv 30 > gpurun_out/launch_summary.txt 2>&1; head -6 gpurun_out/launch_summary.txt
 NCU_SPECS="round_i8:k_round_i8:7 energy16:k_energy_tc:1 outer_i8:k_outer_i8:7" bash tools/gpu_ncu.sh
+# config D (p = 256) at its stated m = 2^22: a bench line and the launch list
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --p-edge 16 --K 32 --s0 16 --m-total 4194304 --scene 4096 > gpurun_out/bench_D.log 2>&1
+python -c "import json; d=json.loads(open('gpurun_out/bench_D.log').read().strip().splitlines()[-1]); print('bench D', d['value'], d['ms_per_step'], d['phases_ms'])"
+DM=4194304 bash tools/gpu_d_launches.sh > gpurun_out/launches_D22_summary.txt 2>&1; head -8 gpurun_out/launches_D22_summary.txt
