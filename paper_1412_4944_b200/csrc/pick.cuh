@@ -129,7 +129,7 @@ struct PickScratch {
 // coefficients >= that bound — typically 20-30.  They are compacted to shared
 // memory and ranked exactly (|c| descending, index ascending: the rule of
 // pick_row_rank) in float64; more than 64 candidates fall back to pick_row.
-__device__ inline RowPick pick_row_cand(const double* Cs, int k, int kind, PickScratch& w) {
+__device__ inline RowPick pick_row_cand64(const double* Cs, int k, int kind, PickScratch& w) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
   double a[8];
@@ -159,6 +159,7 @@ __device__ inline RowPick pick_row_cand(const double* Cs, int k, int kind, PickS
     n += __popc(bal[t]);
   }
   if (n > 64) return pick_row(Cs, 256, k, kind);
+  __syncwarp();
   if (lane < 8) w.bm[lane] = 0u;
   int base = 0;
 #pragma unroll
@@ -184,6 +185,91 @@ __device__ inline RowPick pick_row_cand(const double* Cs, int k, int kind, PickS
       }
       if (rank < k) atomicOr(&w.bm[id >> 5], 1u << (id & 31));
     }
+  }
+  __syncwarp();
+  RowPick r;
+  r.sel = 0u;
+  double sq = 0.0, sc = 0.0, rest = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if ((w.bm[t] >> lane) & 1u) {
+      r.sel |= 1u << t;
+      sq = fma(a[t], a[t], sq);
+      sc += a[t];
+    } else {
+      rest = fma(a[t], a[t], rest);
+    }
+  }
+  __syncwarp();  // the scratch is reused by the warp's next row
+  r.score = warp_sum(kind == SBO_KIND_SQUARED_SUM ? sq : sc);
+  r.rest_sq = warp_sum(rest);
+  return r;
+}
+
+// The same with 32-bit keys (|c| rounded toward zero to float32: monotone, so the
+// bound from the lane maxima still admits every kept coefficient): the bound by a
+// bitonic sort of integer keys, the candidates (at most 32, one per lane, in
+// index order) ranked by shuffles.  When the kept set's smallest key is shared
+// with a discarded candidate, the float32 keys cannot order them: pick_row_cand64
+// decides (exact float64 ranking).
+__device__ inline RowPick pick_row_cand(const double* Cs, int k, int kind, PickScratch& w) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+  double a[8];
+  uint32_t key[8];
+  uint32_t lm = 0u;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    a[t] = fabs(Cs[lane + 32 * t]);
+    key[t] = __float_as_uint(__double2float_rz(a[t]));
+    lm = max(lm, key[t]);
+  }
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint32_t o = __shfl_xor_sync(full, lm, stride);
+      const bool desc = size == 32 || (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      lm = (lower == desc) ? max(lm, o) : min(lm, o);
+    }
+  }
+  const uint32_t lo = __shfl_sync(full, lm, k - 1);
+  unsigned bal[8];
+  int n = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    bal[t] = __ballot_sync(full, key[t] >= lo);
+    n += __popc(bal[t]);
+  }
+  if (n > 32) return pick_row_cand64(Cs, k, kind, w);
+  // compaction in index order (index = lane + 32 t: t-major, lanes ascending)
+  __syncwarp();
+  int base = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if ((bal[t] >> lane) & 1u) {
+      const int at = base + __popc(bal[t] & lt);
+      w.i[at] = static_cast<int16_t>(lane + 32 * t);
+      reinterpret_cast<uint32_t*>(w.v)[at] = key[t];
+    }
+    base += __popc(bal[t]);
+  }
+  if (lane < 8) w.bm[lane] = 0u;
+  __syncwarp();
+  const bool has = lane < n;
+  const uint32_t ck = has ? reinterpret_cast<const uint32_t*>(w.v)[lane] : 0u;
+  int rank = 0;
+  for (int j = 0; j < n; ++j) {
+    const uint32_t kj = __shfl_sync(full, ck, j);
+    rank += (kj > ck) || (kj == ck && j < lane);
+  }
+  const bool sel = has && rank < k;
+  const uint32_t tmin = __reduce_min_sync(full, sel ? ck : 0xffffffffu);
+  if (__any_sync(full, has && !sel && ck == tmin)) return pick_row_cand64(Cs, k, kind, w);
+  if (sel) {
+    const int id = w.i[lane];
+    atomicOr(&w.bm[id >> 5], 1u << (id & 31));
   }
   __syncwarp();
   RowPick r;
