@@ -127,6 +127,106 @@ __global__ void __launch_bounds__(TT * 4) k_ns_gemm(const double* __restrict__ A
   }
 }
 
+// The 64 x 64 tile GEMM with its K chunks (32 wide) double-buffered by cp.async:
+// the next chunk streams from L2 while the current one runs on DMMA.  op(A) for
+// TRANS_A is staged untransposed ([k][i], rows of A) and read transposed.
+// Strides keep every fragment read at the 2-wavefront minimum.
+constexpr int KC = 32, LDA_N = KC + 4, LDA_T = T + 8, LDB = T + 8;
+constexpr int STAGE_DBL = (T * LDA_N > KC * LDA_T ? T * LDA_N : KC * LDA_T) + KC * LDB;
+constexpr size_t PIPE_SMEM = 2 * STAGE_DBL * sizeof(double);
+
+__device__ __forceinline__ void cp16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src));
+}
+
+template <bool TRANS_A, int EPI>
+__global__ void __launch_bounds__(256) k_ns_gemm_pipe(const double* __restrict__ A,
+                                                      const double* __restrict__ B, double* C,
+                                                      int p, int PP, const int* __restrict__ done,
+                                                      double c1, double c3, double* part) {
+  const int b = blockIdx.y;
+  if (done[b]) return;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  double* stage[2] = {reinterpret_cast<double*>(dyn),
+                      reinterpret_cast<double*>(dyn) + STAGE_DBL};
+  __shared__ double red[32];
+  const int nt = PP / T;
+  const int ti = blockIdx.x / nt, tj = blockIdx.x % nt;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int64_t off = static_cast<int64_t>(b) * PP * PP;
+  const double* Ab = A + off;
+  const double* Bb = B + off;
+  constexpr int A_DBL = T * LDA_N > KC * LDA_T ? T * LDA_N : KC * LDA_T;
+  auto issue = [&](int kc, double* st) {
+    double* sA = st;
+    double* sB = st + A_DBL;
+    // 1024 16-B pieces per operand, 4 per thread
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + 256 * u;
+      if (TRANS_A) {  // rows k = kc .. kc + 31 of A, columns ti*T .. + 63
+        const int r = e >> 5, c = 2 * (e & 31);
+        cp16(sA + r * LDA_T + c, Ab + static_cast<int64_t>(kc + r) * PP + ti * T + c);
+      } else {        // rows i = ti*T .. + 63 of A, columns kc .. kc + 31
+        const int r = e >> 4, c = 2 * (e & 15);
+        cp16(sA + r * LDA_N + c, Ab + static_cast<int64_t>(ti * T + r) * PP + kc + c);
+      }
+      const int rb = e >> 5, cb = 2 * (e & 31);
+      cp16(sB + rb * LDB + cb, Bb + static_cast<int64_t>(kc + rb) * PP + tj * T + cb);
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  double acc[8][2];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = 0.0;
+  const int nk = PP / KC;
+  issue(0, stage[0]);
+  for (int c = 0; c < nk; ++c) {
+    if (c + 1 < nk) {
+      issue((c + 1) * KC, stage[(c + 1) & 1]);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* sA = stage[c & 1];
+    const double* sB = sA + A_DBL;
+#pragma unroll
+    for (int k0 = 0; k0 < KC; k0 += 4) {
+      const double a = TRANS_A ? sA[(k0 + t4) * LDA_T + 8 * warp + g]
+                               : sA[(8 * warp + g) * LDA_N + k0 + t4];
+      const double* bb = sB + (k0 + t4) * LDB + g;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) dmma(acc[n][0], acc[n][1], a, bb[8 * n]);
+    }
+    __syncthreads();  // the stage is refilled two chunks later
+  }
+  const int row = ti * T + 8 * warp + g;
+  double dsum = 0.0;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = tj * T + 8 * n + 2 * t4 + h;
+      double v = acc[n][h];
+      if (EPI == 1) {
+        const double delta = row == col ? 1.0 : 0.0;
+        if (row < p && col < p) dsum = fma(v - delta, v - delta, dsum);
+        v = c3 * v + c1 * delta;
+      }
+      acc[n][h] = v;
+    }
+    *reinterpret_cast<double2*>(C + off + static_cast<int64_t>(row) * PP + tj * T + 8 * n +
+                                2 * t4) = make_double2(acc[n][0], acc[n][1]);
+  }
+  if (EPI == 1) {
+    dsum = block_sum<256>(dsum, red);
+    if (tid == 0) part[static_cast<int64_t>(b) * nt * nt + blockIdx.x] = dsum;
+  }
+}
+
 // retire converged matrices: ||X_k^T X_k - I||_F < tol (parts summed in tile order)
 __global__ void k_ns_check(const double* __restrict__ part, int ntile2, int K, int cur, int it,
                            int* done, int* final_buf, int* iters) {
@@ -187,9 +287,11 @@ int sbo_polar_ns_big(const double* P, int K, int p, const int64_t* counts, doubl
   const bool small = K <= 4;
   const int TT = small ? 32 : pbig::T, ntt = PP / TT;
   const dim3 grid(static_cast<unsigned>(ntt * ntt), static_cast<unsigned>(K));
-  const int smem = static_cast<int>(2 * pbig::T * pbig::LDS * sizeof(double));
-  auto g1 = small ? pbig::k_ns_gemm<true, 1, 32> : pbig::k_ns_gemm<true, 1, 64>;
-  auto g0 = small ? pbig::k_ns_gemm<false, 0, 32> : pbig::k_ns_gemm<false, 0, 64>;
+  // larger batches: the cp.async-pipelined 64 x 64 GEMM
+  const int smem = small ? static_cast<int>(2 * pbig::T * pbig::LDS * sizeof(double))
+                         : static_cast<int>(pbig::PIPE_SMEM);
+  auto g1 = small ? pbig::k_ns_gemm<true, 1, 32> : pbig::k_ns_gemm_pipe<true, 1>;
+  auto g0 = small ? pbig::k_ns_gemm<false, 0, 32> : pbig::k_ns_gemm_pipe<false, 0>;
   cudaFuncSetAttribute(g1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(g0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // lower bound of sigma_min / ||P||_F for the scaling (a ratio below it only costs
