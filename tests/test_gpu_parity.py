@@ -452,3 +452,23 @@ def test_graph_replayed_iteration_matches_eager(dev):
         np.testing.assert_array_equal(eng.state.best.cpu().numpy(), want[1])
         np.testing.assert_array_equal(eng.state.residual.cpu().numpy(), want[2])
         assert out.rmse == ref.rmse and out.K == ref.K
+
+
+def test_p0_above_m_samples_with_replacement():
+    """Reference test_sbo.py:272-280 (sbo.py:275-280, 326-329): p0 > m samples
+    the start-up columns with replacement — sbo_init warns, sbo_train notes it
+    in the report instead (it silences sbo_init's warning) — and the trajectory
+    equals the oracle's (which draws the same columns)."""
+    import warnings
+    y = np.random.default_rng(31).standard_normal((6, 40))
+    cfg = S.SboConfig(s0=2, k0=2, p0=100, k_max=3, seed=11, rounds=2)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        d, _, _, rep = S.sbo_train(y, cfg)
+    assert any("replacement" in n for n in rep.notes)
+    blocks, _, rmses, _ = O.train(y, 2, k0=2, p0=100, rounds=2, k_max=3, seed=11)
+    np.testing.assert_allclose([r.rmse for r in rep.rows], rmses, rtol=1e-10)
+    with pytest.warns(UserWarning, match="replacement"):
+        d0 = S.sbo_init(y, cfg)
+    for q in d0.blocks:
+        assert S.orthonormality_defect(q) <= 1e-8
