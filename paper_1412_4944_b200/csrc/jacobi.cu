@@ -143,6 +143,87 @@ __device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) 
   return -1;
 }
 
+// p = 64 sweeps without V on LP lanes per column pair (32 LP threads, the
+// CTA's first warps; the rest wait at the final __syncthreads).  The one-CTA
+// init is issue-bound with 16 lanes per pair: 16 warps x ~185 instructions per
+// tournament step on 4 schedulers.  With LP = 4 one warp per scheduler carries 8
+// pairs of 16 rows each, so a step costs its dependency chain instead.  Lane lg
+// of pair q reads rows LP ((u + q) mod R) + lg (a rotation of the row blocks per
+// pair), so the 32 / LP pairs of a warp hit distinct banks whatever the columns.
+// Same rotations, schedule and tolerances as jacobi_sweeps64.  Returns the
+// sweep count (or -1) to every thread of the CTA.
+template <int LP>
+__device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result_smem) {
+  constexpr int N = 64, R = N / LP, NT = 32 * LP, PPW = 32 / LP;
+  static_assert(LP == 4 || LP == 8, "4 or 8 lanes per pair");
+  const int tid = threadIdx.x;
+  if (tid < NT) {
+    const int q = tid / LP, lg = tid % LP, qw = q % PPW;
+    const double tol2 = DBL_EPSILON * DBL_EPSILON;
+    const double conv = 4.0 * 8.0 * DBL_EPSILON, conv2 = conv * conv;
+    int result = -1;
+    int roff[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) roff[u] = LP * ((u + qw) % R) + lg;
+    for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+      if (tid == 0) *flag = 0;
+      asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+      int i = q, j = q == 0 ? N - 1 : N - 1 - q;
+      for (int step = 0; step < N - 1; ++step) {
+        double* ai = A + i * N;
+        double* aj = A + j * N;
+        double x[R], y[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+          x[u] = ai[roff[u]];
+          y[u] = aj[roff[u]];
+        }
+        // two accumulator chains per sum (half the dependent DFMA depth)
+        double al0 = 0.0, al1 = 0.0, be0 = 0.0, be1 = 0.0, ga0 = 0.0, ga1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < R; u += 2) {
+          al0 = fma(x[u], x[u], al0);
+          be0 = fma(y[u], y[u], be0);
+          ga0 = fma(x[u], y[u], ga0);
+          al1 = fma(x[u + 1], x[u + 1], al1);
+          be1 = fma(y[u + 1], y[u + 1], be1);
+          ga1 = fma(x[u + 1], y[u + 1], ga1);
+        }
+        double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+#pragma unroll
+        for (int o = LP / 2; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        const double g2 = ga * ga, ab = al * be;
+        if (al > 0.0 && be > 0.0 && g2 > tol2 * ab) {
+          double c, sn;
+          rotation(al, be, ga, c, sn);
+#pragma unroll
+          for (int u = 0; u < R; ++u) {
+            ai[roff[u]] = c * x[u] - sn * y[u];
+            aj[roff[u]] = sn * x[u] + c * y[u];
+          }
+          if (lg == 0 && g2 > conv2 * ab) *flag = 1;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+        // next step: i, j advance by one modulo 63 (slot 0 keeps j = 63)
+        i = (i == N - 2) ? 0 : i + 1;
+        if (q != 0) j = (j == N - 2) ? 0 : j + 1;
+      }
+      if (*reinterpret_cast<volatile int*>(flag) == 0) {
+        result = sweep + 1;
+        break;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");  // flag read before reset
+    }
+    if (tid == 0) *result_smem = result;
+  }
+  __syncthreads();
+  return *reinterpret_cast<volatile int*>(result_smem);
+}
+
 // Runs the sweeps on A (p x p, col-major) accumulating V.  Returns the sweep
 // count, or -1 when kMaxSweeps is exhausted.  All threads of the CTA call it.
 __device__ __forceinline__ int jacobi_sweeps(double* A, double* V, int rows, int p, int* flag) {
@@ -390,9 +471,9 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
 }
 
 // ---------------------------------------------------------------------------
-// The same scaled Newton-Schulz iteration spread over a cluster of 4 CTAs per
-// matrix (one per SM), exchanging through distributed shared memory.  CTA r
-// owns the column slice J_r = [16r, 16r+16):
+// The same scaled Newton-Schulz iteration spread over a cluster of NC = 4 or 8
+// CTAs per matrix (one per SM), exchanging through distributed shared memory.
+// CTA r owns the column slice J_r = [W r, W r + W), W = 64 / NC:
 //   G rows J_r    = X[:, J_r]^T X                         (local, full X held)
 //   A cols J_r    = c1 I + c3 G[J_r, :]^T                 (G symmetric: local)
 //   X' cols J_r   = X A[:, J_r]                           (local)
@@ -406,7 +487,6 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar_ns(const double* __res
 // meanwhile, so a converged X_k is still in the other buffer.  All CTAs take identical decisions
 // (same partial sums in the same order), so the cluster leaves the loop together.
 // ---------------------------------------------------------------------------
-constexpr int kNsCluster = 4;
 
 // DSMEM helpers: shared::cluster addresses and cluster-scope release/acquire
 // (generic stores would make the barrier fence at GPU scope)
@@ -421,13 +501,11 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// X is held slice-major: Xs[q][k][c] = X[k][16q + c] with a 20-double row stride
-// (conflict-free DMMA fragments), so a CTA's slice is one contiguous 10-KB block
+// X is held slice-major: Xs[q][k][c] = X[k][W q + c] with a W + 4 double row stride
+// (conflict-free DMMA fragments), so a CTA's slice is one contiguous block
 // that a single cp.async.bulk shared::cta -> shared::cluster copy delivers to a
-// peer (completing on the peer's mbarrier).  The slice's padding column 16 of
+// peer (completing on the peer's mbarrier).  The slice's padding column W of
 // row 0 carries the CTA's deviation partial.
-constexpr int kNsSliceLd = 64 / kNsCluster + 4;  // slice columns + 4: conflict-free fragments
-constexpr int kNsSlice = 64 * kNsSliceLd;  // doubles per slice
 
 __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, uint32_t bytes,
                                                uint32_t mbar) {
@@ -437,19 +515,21 @@ __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, ui
       : "memory");
 }
 
-__global__ void __cluster_dims__(kNsCluster, 1, 1) __launch_bounds__(kJacobiThreads)
+template <int NC>
+__global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(kJacobiThreads)
     k_polar_ns_cluster(const double* __restrict__ P, const int64_t* __restrict__ counts,
                        double* Q, int32_t* status, double l0) {
-  constexpr int N = 64, NC = kNsCluster, W = N / NC, SL = kNsSliceLd, SZ = kNsSlice;
+  // slice row stride: slice columns + 4 (conflict-free fragments)
+  constexpr int N = 64, W = N / NC, SL = W + 4, SZ = 64 * SL;
   constexpr int A2 = W / 8;  // 8-column tiles per slice
   static_assert(W % 8 == 0 && (SL % 16 == 4 || SL % 16 == 12), "slice layout");
   const int r = static_cast<int>(blockIdx.x % NC);  // == %cluster_ctarank for 1-D clusters
   const int b = blockIdx.x / NC;
   __shared__ double red[32];
   __shared__ __align__(8) uint64_t full[2];
-  extern __shared__ __align__(128) unsigned char dyn[];
-  double* X0 = reinterpret_cast<double*>(dyn);  // buffer u, slice q: X0 + (u * NC + q) * SZ
-  constexpr int AL = kNsSliceLd;
+  extern __shared__ __align__(128) unsigned char dyn_ns[];
+  double* X0 = reinterpret_cast<double*>(dyn_ns);  // buffer u, slice q: X0 + (u * NC + q) * SZ
+  constexpr int AL = SL;
   double* As = X0 + 2 * NC * SZ;                // A[:, J_r] as As[j][i] (stride AL)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   if (counts && counts[b] == 0) {
@@ -717,7 +797,7 @@ __global__ void __launch_bounds__(kJacobiThreads) k_polar(const double* __restri
 // caller's rank test drops them and completes the basis).  512 threads.
 // Out: V col-major eigenvectors (unordered), lam[j] = sigma_j^2.  Returns sweeps.
 __device__ int init_eig64_precond(const double* __restrict__ G, double* A, double* V,
-                                  double* W, double* lam, int* perm, int* flag) {
+                                  double* W, double* lam, int* perm, int* flag, int lp) {
   constexpr int N = 64, LDW = 65;
   const int tid = threadIdx.x;
   __shared__ int piv;
@@ -795,7 +875,10 @@ __device__ int init_eig64_precond(const double* __restrict__ G, double* A, doubl
     A[e] = (j < rank && r >= j) ? W[j * LDW + r] : 0.0;
   }
   __syncthreads();
-  const int sweeps = jacobi_sweeps64<512>(A, nullptr, flag);
+  __shared__ int sweeps_smem;
+  const int sweeps = lp == 4   ? jacobi_sweeps64_lp<4>(A, flag, &sweeps_smem)
+                     : lp == 8 ? jacobi_sweeps64_lp<8>(A, flag, &sweeps_smem)
+                               : jacobi_sweeps64<512>(A, nullptr, flag);
   // sigma_j = ||A_j||; eigenvector j of G = P (A_j / sigma_j)
   if (tid < N) {
     double ss = 0.0;
@@ -899,7 +982,7 @@ template <bool SMEM, int NT>
 __global__ void __launch_bounds__(NT) k_init_block(
     const double* __restrict__ G, int p, int64_t ncols, const double* __restrict__ draws,
     int ndraws, double* Q, int32_t* rank_out, int32_t* status, double* ws, int use_smem,
-    const int* presolved_sweeps = nullptr) {
+    const int* presolved_sweeps, int lp) {
   const int64_t pp = static_cast<int64_t>(p) * p;
   __shared__ JacobiSmem S;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -918,7 +1001,7 @@ __global__ void __launch_bounds__(NT) k_init_block(
   if constexpr (SMEM && NT == 512) {
     if (p == 64 && !presolved_sweeps) {
       __shared__ int permv[64];
-      sweeps = init_eig64_precond(G, A, V, U, lam, permv, &S.flag);
+      sweeps = init_eig64_precond(G, A, V, U, lam, permv, &S.flag, lp);
       lam_ready = true;
     }
   }
@@ -1074,8 +1157,30 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
       // > half of an SM's shared memory: one CTA per SM, so the 8 CTAs of a
       // cluster run on 8 SMs (they would otherwise pack 3 to an SM)
       const size_t nsb = 120 * 1024;
-      cudaFuncSetAttribute(k_polar_ns_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_polar_ns_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(nsb));
+      cudaFuncSetAttribute(k_polar_ns_cluster<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(nsb));
+      // 8-CTA clusters (half the DMMA work per SM per iteration) when all K of them
+      // are co-resident; otherwise 4 (a second wave would cost more than it saves).
+      // SBO_NS_CLUSTER = 4 or 8 forces the size.
+      static const int max8 = [nsb] {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(8, 1, 1);
+        cfg.blockDim = dim3(kJacobiThreads, 1, 1);
+        cfg.dynamicSmemBytes = nsb;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_polar_ns_cluster<8>, &cfg) != cudaSuccess) {
+          cudaGetLastError();
+          n = 0;
+        }
+        return n;
+      }();
+      static const int force = [] {
+        const char* e = std::getenv("SBO_NS_CLUSTER");
+        return e ? std::atoi(e) : 0;
+      }();
+      const bool c8 = force == 8 || (force != 4 && K <= max8);
       // Chen-Chow lower bound l0 for sigma_min(P) / ||P||_F: on the benchmark's patch
       // data the P matrices have ratios ~1e-5 .. 1e-4, where l0 = 1e-5 converges in
       // 17 iterations (1e-6: 19; 1e-4: 19-20; 1e-3: 23).  A ratio below l0 only
@@ -1085,8 +1190,12 @@ extern "C" int sbo_polar(const double* P, int K, int p, const int64_t* counts, d
         const char* e = std::getenv("SBO_NS_L0");
         return e ? std::atof(e) : 1e-5;
       }();
-      k_polar_ns_cluster<<<K * kNsCluster, kJacobiThreads, nsb, as_stream(stream)>>>(
-          P, counts, Q, status, l0);
+      if (c8)
+        k_polar_ns_cluster<8><<<K * 8, kJacobiThreads, nsb, as_stream(stream)>>>(P, counts, Q,
+                                                                               status, l0);
+      else
+        k_polar_ns_cluster<4><<<K * 4, kJacobiThreads, nsb, as_stream(stream)>>>(P, counts, Q,
+                                                                               status, l0);
       if (int rc = check_launch("k_polar_ns_cluster")) return rc;
     }
   }
@@ -1116,13 +1225,19 @@ extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const doubl
     if (p == 64) {  // 512 threads: one column pair per half-warp (jacobi_sweeps64)
       cudaFuncSetAttribute(k_init_block<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(dyn));
+      // lanes per Jacobi column pair (jacobi_sweeps64_lp); SBO_INIT_LP = 16 selects
+      // the 512-thread jacobi_sweeps64 (A/B)
+      static const int lp = [] {
+        const char* e = std::getenv("SBO_INIT_LP");
+        return e ? std::atoi(e) : 8;
+      }();
       k_init_block<true, 512><<<1, 512, dyn, as_stream(stream)>>>(
-          G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
+          G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1, nullptr, lp);
     } else {
       cudaFuncSetAttribute(k_init_block<true, kJacobiThreads>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
       k_init_block<true, kJacobiThreads><<<1, kJacobiThreads, dyn, as_stream(stream)>>>(
-          G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1);
+          G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 1, nullptr, 16);
     }
   } else {
     // large p: the sweeps on a cooperative grid, then the single-CTA finish
@@ -1141,7 +1256,7 @@ extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const doubl
     SBO_CHECK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_jacobi_grid), blocks,
                                                256, args, 0, as_stream(stream)));
     k_init_block<false, kJacobiThreads><<<1, kJacobiThreads, 0, as_stream(stream)>>>(
-        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 0, sweeps);
+        G, p, ncols, draws, ndraws, Q, rank, status, static_cast<double*>(ws), 0, sweeps, 16);
   }
   return check_launch("k_init_block");
 }
