@@ -153,8 +153,7 @@ __device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) 
 // Same rotations, schedule and tolerances as jacobi_sweeps64.  Returns the
 // sweep count (or -1) to every thread of the CTA.
 template <int LP>
-__device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result_smem,
-                                               bool early) {
+__device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result_smem) {
   constexpr int N = 64, R = N / LP, NT = 32 * LP, PPW = 32 / LP;
   static_assert(LP == 4 || LP == 8, "4 or 8 lanes per pair");
   const int tid = threadIdx.x;
@@ -162,16 +161,12 @@ __device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result
     const int q = tid / LP, lg = tid % LP, qw = q % PPW;
     const double tol2 = DBL_EPSILON * DBL_EPSILON;
     const double conv = 4.0 * 8.0 * DBL_EPSILON, conv2 = conv * conv;
-    // early exit: a sweep whose every rotation had |gamma| <= 1e-9 sqrt(alpha beta)
-    // leaves off-diagonal ratios ~ n 1e-18, far below conv, so the confirming sweep
-    // (which would rotate nothing above conv) is skipped
-    const double tiny2 = early ? 1e-18 : 0.0;
     int result = -1;
     int roff[R];
 #pragma unroll
     for (int u = 0; u < R; ++u) roff[u] = LP * ((u + qw) % R) + lg;
     for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
-      if (tid == 0) flag[0] = flag[1] = 0;
+      if (tid == 0) *flag = 0;
       asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
       int i = q, j = q == 0 ? N - 1 : N - 1 - q;
       for (int step = 0; step < N - 1; ++step) {
@@ -210,20 +205,18 @@ __device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result
             ai[roff[u]] = c * x[u] - sn * y[u];
             aj[roff[u]] = sn * x[u] + c * y[u];
           }
-          if (lg == 0 && g2 > conv2 * ab) flag[0] = 1;
-          if (lg == 0 && g2 > tiny2 * ab) flag[1] = 1;
+          if (lg == 0 && g2 > conv2 * ab) *flag = 1;
         }
         asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
         // next step: i, j advance by one modulo 63 (slot 0 keeps j = 63)
         i = (i == N - 2) ? 0 : i + 1;
         if (q != 0) j = (j == N - 2) ? 0 : j + 1;
       }
-      const volatile int* vf = flag;
-      if (vf[0] == 0 || vf[1] == 0) {
+      if (*reinterpret_cast<volatile int*>(flag) == 0) {
         result = sweep + 1;
         break;
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");  // flags read before reset
+      asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");  // flag read before reset
     }
     if (tid == 0) *result_smem = result;
   }
@@ -883,12 +876,9 @@ __device__ int init_eig64_precond(const double* __restrict__ G, double* A, doubl
   }
   __syncthreads();
   __shared__ int sweeps_smem;
-  __shared__ int flags2[2];
-  const bool early = lp > 0;  // lp < 0: the same lanes without the early exit (A/B)
-  const int lpa = lp < 0 ? -lp : lp;
-  const int sweeps = lpa == 4   ? jacobi_sweeps64_lp<4>(A, flags2, &sweeps_smem, early)
-                     : lpa == 8 ? jacobi_sweeps64_lp<8>(A, flags2, &sweeps_smem, early)
-                                : jacobi_sweeps64<512>(A, nullptr, flag);
+  const int sweeps = lp == 4   ? jacobi_sweeps64_lp<4>(A, flag, &sweeps_smem)
+                     : lp == 8 ? jacobi_sweeps64_lp<8>(A, flag, &sweeps_smem)
+                               : jacobi_sweeps64<512>(A, nullptr, flag);
   // sigma_j = ||A_j||; eigenvector j of G = P (A_j / sigma_j)
   if (tid < N) {
     double ss = 0.0;
@@ -1236,8 +1226,7 @@ extern "C" int sbo_init_block(const double* G, int p, int64_t ncols, const doubl
       cudaFuncSetAttribute(k_init_block<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(dyn));
       // lanes per Jacobi column pair (jacobi_sweeps64_lp); SBO_INIT_LP = 16 selects
-      // the 512-thread jacobi_sweeps64, -4 / -8 the narrow sweeps without the early
-      // exit (A/B)
+      // the 512-thread jacobi_sweeps64 (A/B)
       static const int lp = [] {
         const char* e = std::getenv("SBO_INIT_LP");
         return e ? std::atoi(e) : 8;
