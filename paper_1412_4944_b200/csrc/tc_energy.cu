@@ -68,9 +68,12 @@ struct Ring {
   }
 };
 
-// error model of one coefficient (absolute, unscaled units), see DESIGN.md:
-// split representation 3 * 2^-22 and fp32 accumulation of 192 exact products
-__device__ __forceinline__ float coef_err(float s_norm) { return 2.5e-6f * sqrtf(s_norm); }
+// error model of one coefficient (absolute, unscaled units), see DESIGN.md section 3:
+// split representation 3 * 2^-22 and 12 MMAs that each truncate toward zero into the
+// fp32 accumulator (measured, tools/f16acc_micro.cu): (12 * 2^-23 + 3 * 2^-22) ||y||
+// = 2.15e-6 ||y||, with margin (2.5e-6 before round 2's measurement: +19 % flagged
+// signals at 3.0e-6, no measurable time)
+__device__ __forceinline__ float coef_err(float s_norm) { return 3.0e-6f * sqrtf(s_norm); }
 
 // bound on |R_hat - R| for a block with n discarded coefficients: coefficient
 // errors (Cauchy-Schwarz over the discarded set, which may differ from the exact
