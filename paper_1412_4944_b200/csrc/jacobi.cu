@@ -54,6 +54,34 @@ __device__ __forceinline__ void rotation(double al, double be, double ga, double
   s = c * t;
 }
 
+// The same rotation with approximate fp32 MUFU square root / reciprocal for the
+// angle (a few ulp, like the fp32 angle itself) and c = (1 + t^2)^-1/2 from the
+// float64 MUFU estimate refined by two Newton steps (to rounding, so c^2 + s^2 = 1
+// as before): a shorter dependent chain than the IEEE sqrt / div / rsqrt paths.
+__device__ __forceinline__ void rotation_fast(double al, double be, double ga, double& c,
+                                              double& s) {
+  const double d = be - al, gg = 2.0 * ga;
+  const int hi = __double2hiint(fmax(fabs(d), fabs(gg)));
+  const int e = ((hi >> 20) & 0x7ff) - 1023;
+  const double scale = __hiloint2double((1023 - e) << 20, 0);
+  const float df = static_cast<float>(d * scale);
+  const float gf = static_cast<float>(gg * scale);
+  const float h2 = fmaf(df, df, gf * gf);
+  const float h = h2 * rsqrtf(h2);
+  const float tf = copysignf(1.0f, df) * __fdividef(gf, fabsf(df) + h);
+  const double t = static_cast<double>(tf);
+  const double x = fma(t, t, 1.0);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double r = fma(-x * y, y, 1.0);
+    y = fma(0.5 * y, r, y);
+  }
+  c = y;
+  s = c * t;
+}
+
 // p = 64 specialization: 32 column pairs per step.  A half-warp (16 lanes) owns a
 // pair, so each shared-memory access reads 16 consecutive rows of ONE column —
 // conflict-free whatever the columns (8 lanes per pair put 4 columns of equal
@@ -153,7 +181,8 @@ __device__ __forceinline__ int jacobi_sweeps64(double* A, double* V, int* flag) 
 // Same rotations, schedule and tolerances as jacobi_sweeps64.  Returns the
 // sweep count (or -1) to every thread of the CTA.
 template <int LP>
-__device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result_smem) {
+__device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result_smem,
+                                               bool fast) {
   constexpr int N = 64, R = N / LP, NT = 32 * LP, PPW = 32 / LP;
   static_assert(LP == 4 || LP == 8, "4 or 8 lanes per pair");
   const int tid = threadIdx.x;
@@ -199,7 +228,8 @@ __device__ __noinline__ int jacobi_sweeps64_lp(double* A, int* flag, int* result
         const double g2 = ga * ga, ab = al * be;
         if (al > 0.0 && be > 0.0 && g2 > tol2 * ab) {
           double c, sn;
-          rotation(al, be, ga, c, sn);
+          if (fast) rotation_fast(al, be, ga, c, sn);
+          else rotation(al, be, ga, c, sn);
 #pragma unroll
           for (int u = 0; u < R; ++u) {
             ai[roff[u]] = c * x[u] - sn * y[u];
@@ -876,9 +906,11 @@ __device__ int init_eig64_precond(const double* __restrict__ G, double* A, doubl
   }
   __syncthreads();
   __shared__ int sweeps_smem;
-  const int sweeps = lp == 4   ? jacobi_sweeps64_lp<4>(A, flag, &sweeps_smem)
-                     : lp == 8 ? jacobi_sweeps64_lp<8>(A, flag, &sweeps_smem)
-                               : jacobi_sweeps64<512>(A, nullptr, flag);
+  const bool fast = lp > 0;  // lp < 0: the same lanes with the IEEE rotation (A/B)
+  const int lpa = lp < 0 ? -lp : lp;
+  const int sweeps = lpa == 4   ? jacobi_sweeps64_lp<4>(A, flag, &sweeps_smem, fast)
+                     : lpa == 8 ? jacobi_sweeps64_lp<8>(A, flag, &sweeps_smem, fast)
+                                : jacobi_sweeps64<512>(A, nullptr, flag);
   // sigma_j = ||A_j||; eigenvector j of G = P (A_j / sigma_j)
   if (tid < N) {
     double ss = 0.0;
