@@ -100,9 +100,9 @@ static float mma_model(float acc, const __float128* p, int F, bool trunc_acc) {
   return to_f32_rz(s);
 }
 
-int main() {
+int main(int argc, char** argv) {
   std::vector<__half> A(M * KT), B(N * KT);
-  srand(11);
+  srand(argc > 1 ? std::atoi(argv[1]) : 11);
   auto rnd_mixed = [] {
     // +-(1 + f) 2^e, e in [-12, 0], 10-bit f: exact fp16 normals
     const int e = -(rand() % 13);
@@ -157,6 +157,13 @@ int main() {
   if (cudaMemcpy(O.data(), dO, O.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
     printf("error %s\n", cudaGetErrorString(cudaGetLastError()));
     return 1;
+  }
+  // raw dump for offline model fitting: A (M x KT fp16 bits), B (N x KT), D (M x N fp32)
+  if (FILE* f = std::fopen(argc > 2 ? argv[2] : "gpurun_out/f16acc.bin", "wb")) {
+    std::fwrite(A.data(), 2, A.size(), f);
+    std::fwrite(B.data(), 2, B.size(), f);
+    std::fwrite(O.data(), 4, O.size(), f);
+    std::fclose(f);
   }
   long match_e = 0, match_z = 0, total = 0;
   constexpr int NF = 10;  // F = 23 .. 32
