@@ -7,7 +7,11 @@ SRC       := $(wildcard $(PKG)/csrc/*.cu)
 OBJ       := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB       := $(PKG)/libsbo_b200.so
 
-all: $(LIB)
+all: $(LIB) tools/f16acc_micro
+
+# the tensor-core accumulation probe behind the energy pass's certificate (tests/test_gpu_f16acc.py)
+tools/f16acc_micro: tools/f16acc_micro.cu $(PKG)/csrc/sm100.cuh
+	$(NVCC) $(ARCH) -O2 -std=c++17 -I$(PKG)/csrc -o $@ $<
 
 build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/sbo_b200.h
 	@mkdir -p build
@@ -17,6 +21,6 @@ $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) tools/f16acc_micro
 
 .PHONY: all clean
